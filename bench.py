@@ -1,0 +1,283 @@
+#!/usr/bin/env python
+"""Benchmark of the KPM-DOS hot path (BASELINE.json metric: augmented SpMMV Gflop/s,
+complex double, at R=1..32, with the fraction of the HBM roofline).
+
+A step = one full kpm_moments call = the whole hot path of SURVEY §8(a): Z4 start block,
+init sweep, M/2-1 augmented SpMMV sweeps with fused dot products, the eta reduction and
+the eta -> mu step.  Workload at N GPUs: the TI lattice (200*N) x 100 x 40 ("Bar" weak
+scaling of P:904-905; at N=1 exactly config C3 = the paper's single-device domain
+200x100x40), M=2000, R=32.
+
+Gflop/s uses the paper's algorithmic flop count (Table I):
+    flops = (M/2) * R * (8 N_nz + 34 N)
+and the roofline the paper's minimum traffic (Eq. (8) `eq:traffic_kpm_improved_blocked`):
+    bytes per sweep = N_nz (S_d + S_i) + 3 R S_d N = 20 N_nz + 48 R N.
+
+`--impl reference` times the oracle (plain CPU KPM, oracle/) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads.ti_lattice import SEED, Lattice, gershgorin, generate_csr, scale_factors  # noqa: E402
+
+S_D, S_I = 16, 4
+
+
+def alg_flops_per_sweep(n, nnz, R):
+    return R * (8 * nnz + 34 * n)
+
+
+def alg_bytes_per_sweep(n, nnz, R):
+    return nnz * (S_D + S_I) + 3 * R * S_D * n
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        rows = [l.strip().split(", ") for l in self.f.read().splitlines() if l.strip()]
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip() == "Active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def build_problem(nx, ny, nz):
+    lat = Lattice(nx, ny, nz)
+    rp, col, val = generate_csr(lat)
+    a, b = scale_factors(*gershgorin(rp, col, val))
+    return lat, rp, col, val, a, b
+
+
+def oracle_sample(rp, col, val, a, b, n, nnz, target_s=15.0, max_sweeps=400):
+    """Time the oracle (as it stands) on a bounded sample: 1 random vector, S sweeps."""
+    import oracle
+
+    threads = host_cores()
+    t0 = time.perf_counter()
+    oracle.kpm_eta(rp, col, val, a, b, 4, 1, SEED, threads=threads)  # 2 sweeps, calibrate
+    t_cal = (time.perf_counter() - t0) / 2
+    sweeps = int(max(2, min(max_sweeps, target_s / max(t_cal, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.kpm_eta(rp, col, val, a, b, 2 * sweeps, 1, SEED, threads=threads)
+    t = time.perf_counter() - t0
+    gf = sweeps * alg_flops_per_sweep(n, nnz, 1) / t / 1e9
+    return gf, threads, sweeps, t
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    nx, ny, nz = 200, 100, 40
+    lat, rp, col, val, a, b = build_problem(nx, ny, nz)
+    nnz = int(rp[-1])
+    threads = host_cores()
+    import oracle
+
+    sweeps = 8
+    for _ in range(args.warmup):
+        oracle.kpm_eta(rp, col, val, a, b, 2 * sweeps, 1, SEED, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.kpm_eta(rp, col, val, a, b, 2 * sweeps, 1, SEED, threads=threads)
+    t = time.perf_counter() - t0
+    value = args.steps * sweeps * alg_flops_per_sweep(lat.n, nnz, 1) / t / 1e9
+    sample = f"C3 lattice {nx}x{ny}x{nz} (N={lat.n}, N_nz={nnz}), 1 random vector, {sweeps} sweeps per step"
+    print(json.dumps({
+        "impl": "reference", "metric": "augmented SpMMV Gflop/s (cplx dbl)", "value": value, "unit": "Gflop/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": "C3 (oracle sample)", "lattice": [nx, ny, nz], "M": 2 * sweeps, "R": 1},
+        "cpu_baseline": {"value": value, "unit": "Gflop/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "Gflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--M", type=int, default=2000)
+    ap.add_argument("--R", type=int, default=32)
+    ap.add_argument("--lattice", default="200,100,40", help="per-GPU x-slab nx,ny,nz")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-r-sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        raise SystemExit("multi-GPU bench not built yet")
+
+    import torch
+
+    import paper_1410_5242_b200 as kpm
+
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
+    nx, ny, nz = (int(t) for t in args.lattice.split(","))
+    nx *= world
+    lat, rp, col, val, a, b = build_problem(nx, ny, nz)
+    n, nnz = lat.n, int(rp[-1])
+    M, R = args.M, args.R
+    ctx = kpm.KpmContext(device=local, cuda_stream=stream.cuda_stream)
+    ctx.set_matrix(rp, col, val, a, b)
+    n_blocks = (R + 31) // 32
+
+    for _ in range(args.warmup):
+        ctx.moments(M, R, SEED)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sweep_ms = []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            mu, _ = ctx.moments(M, R, SEED, want_eta=False)
+            sweep_ms.append(ctx.last_timing()[1])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    clocks = clk.summary()
+    t_ms = ev0.elapsed_time(ev1)
+    flops_step = (M // 2) * alg_flops_per_sweep(n, nnz, R)
+    value = args.steps * flops_step / (t_ms * 1e-3) / 1e9
+    hbm, peak_src = peaks()
+    sweep = statistics.median(sweep_ms)
+    bytes_sweep = alg_bytes_per_sweep(n, nnz, R)
+    achieved = bytes_sweep / (sweep * 1e-3) / 1e9
+    bmin = alg_bytes_per_sweep(n, nnz, R) / alg_flops_per_sweep(n, nnz, R)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get(f"{nx}x{ny}x{nz}/R{R}")
+    out = {
+        "metric": "augmented SpMMV Gflop/s (cplx dbl)", "value": value, "unit": "Gflop/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"C3 TI lattice {nx}x{ny}x{nz} x 4 orbitals, M={M}, R={R}" if world == 1 else
+                   f"Bar TI lattice {nx}x{ny}x{nz}, M={M}, R={R}", "lattice": [nx, ny, nz], "N": n, "N_nz": nnz,
+                   "M": M, "R": R, "parallelism": f"x-slab dp{world}",
+                   "l2": "inputs larger than L2 (V, W %.2f GB each; matrix %.2f GB)" % (
+                       16 * R * n / 1e9, 20 * nnz / 1e9)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "kernel": "aug_spmmv main sweep", "sweep_ms": sweep,
+                     "alg_bytes_per_launch": bytes_sweep, "peak_source": peak_src,
+                     "B_min_bytes_per_flop": bmin, "P_mem_gflops": hbm / bmin,
+                     "kernel_gflops": alg_flops_per_sweep(n, nnz, R) / (sweep * 1e-3) / 1e9},
+        "gpu_launches": args.steps * n_blocks * (M // 2 + 2),
+        "clocks": clocks,
+    }
+    # R sweep of the same lattice (HBM -> cache bottleneck shift), shorter M
+    if not args.no_r_sweep:
+        by_r = {}
+        for r in (1, 2, 4, 8, 16, 32):
+            ctx.moments(200, r, SEED, want_eta=False)
+            ctx.moments(200, r, SEED, want_eta=False)
+            sw = ctx.last_timing()[1]
+            bs = alg_bytes_per_sweep(n, nnz, r)
+            by_r[str(r)] = {"sweep_ms": sw, "gflops": alg_flops_per_sweep(n, nnz, r) / (sw * 1e-3) / 1e9,
+                            "hbm_gbs_alg": bs / (sw * 1e-3) / 1e9, "frac": bs / (sw * 1e-3) / 1e9 / hbm,
+                            "P_mem_gflops": hbm / (bs / alg_flops_per_sweep(n, nnz, r))}
+        out["by_R"] = by_r
+    # e2e: host CSR in, mu/eta out, through the C ABI, copies inside the timed region
+    if not args.no_e2e:
+        h2d = rp.nbytes + col.nbytes + val.nbytes
+        d2h = M * 8 + R * M * 16
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.set_matrix(rp, col, val, a, b)
+            ctx.moments(M, R, SEED, want_eta=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1)
+        out["e2e"] = {"value": args.steps * flops_step / (te * 1e-3) / 1e9, "unit": "Gflop/s",
+                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                      "ms_per_step": te / args.steps,
+                      "note": "kpm_set_matrix(host CSR: validation, SELL build, H2D) + kpm_moments (D2H mu, eta)"}
+    if rank == 0 and not args.no_cpu_baseline:
+        gf, threads, sweeps, t = oracle_sample(rp, col, val, a, b, n, nnz)
+        out["cpu_baseline"] = {"value": gf, "unit": "Gflop/s", "cores": threads, "kind": "oracle",
+                               "sample": f"same lattice, 1 random vector, {sweeps} sweeps ({t:.1f} s)"}
+    ctx.close()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

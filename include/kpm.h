@@ -1,0 +1,144 @@
+/*
+ * kpm.h -- C ABI of the B200-native KPM-DOS hot path (arXiv:1410.5242).
+ *
+ * The library computes the Chebyshev moments of the Kernel Polynomial Method with the
+ * blocked, augmented SpMMV of Fig. 5 `alg:kpm_improved_blocked`:
+ * every sweep applies H~ = a(H - b 1) to a row-major block of R vectors, forms
+ * W <- 2 H~ V - W and the two column-wise scalar products eta_2m = <V|V>,
+ * eta_2m+1 = <W|V> in the same pass over the matrix, so the
+ * matrix is read M/2 times in total.  Moments are reduced across ranks once, at
+ * the end (Table III).
+ *
+ * Conventions shared by every entry point
+ *   - Every function returns kpm_status; nothing throws across the ABI.
+ *   - Complex numbers are interleaved (re, im) doubles.  Block vectors are row-major:
+ *     element (i, r) of an n x R block is at index i*R + r.
+ *   - The caller owns every pointer it passes and may free it when the call returns
+ *     (kpm_set_matrix copies the matrix).  The library owns all device memory it
+ *     allocates; kpm_destroy releases it.
+ *   - Host pointers are plain pageable or pinned memory.  KPM_MEM_DEVICE inputs are
+ *     device pointers on the context's device.
+ *   - On an error the context stays usable, except after KPM_ECUDA / KPM_ENCCL, after
+ *     which only kpm_destroy and kpm_last_error are valid.
+ *   - One host thread per context at a time.
+ *   - nranks > 1: kpm_create, kpm_set_matrix and kpm_moments* are collective: every rank
+ *     calls them in the same order with identical n_global, a, b, M, R, seed; the row
+ *     ranges [row_begin, row_end) tile [0, n_global) in rank order (the data-parallel
+ *     row distribution of P:849-854, equal weights).
+ */
+#ifndef KPM_H
+#define KPM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct kpm_ctx kpm_ctx; /* opaque, owned by the library */
+
+typedef enum {
+  KPM_OK = 0,
+  KPM_EINVAL = 1,     /* bad argument: M odd or < 2, R < 1, a <= 0, non-finite a/b/values,
+                         NULL pointer, malformed CSR, unsupported option                 */
+  KPM_ESTATE = 2,     /* kpm_moments* before kpm_set_matrix                                 */
+  KPM_ERANGE = 3,     /* local rows + halo rows > INT32_MAX (4-byte kernel indices),
+                         or a column outside [0, n_global)                                 */
+  KPM_ENOMEM = 4,     /* device or host allocation failed                                   */
+  KPM_ECUDA = 5,      /* CUDA error (sticky: destroy the context)                           */
+  KPM_ENCCL = 6,      /* NCCL error (sticky)                                                */
+  KPM_EZERONORM = 7,  /* kpm_moments_v0: a start column has eta_0 = <v|v> = 0               */
+  KPM_WDIVERGED = 8   /* warning, results written: some |mu_n| > mu_0 (1 + 1e-8), i.e. a, b do
+                         not map the spectrum into [-1, 1]                          */
+} kpm_status;
+
+enum { KPM_MEM_HOST = 0, KPM_MEM_DEVICE = 1 };
+
+typedef struct {
+  int device;                   /* CUDA device ordinal of this rank                         */
+  int nranks;                   /* >= 1                                                     */
+  int rank;                     /* 0 .. nranks-1                                            */
+  const void* nccl_unique_id;   /* 128-byte ncclUniqueId, identical on all ranks; NULL when
+                                   nranks == 1                                              */
+  void* cuda_stream;            /* cudaStream_t every kernel and copy is issued on, or NULL
+                                   for a library-owned stream                               */
+  int sell_C;                   /* SELL chunk height C; 0 -> 32. Only 32 (= warpSize)
+                                   is supported                                             */
+  int sell_sigma;               /* SELL sorting scope sigma; 0 -> 1 (no sorting). 1 or a
+                                   multiple of C                                            */
+  unsigned flags;               /* reserved, pass 0                                         */
+} kpm_options;
+
+typedef struct {
+  int64_t n_global;             /* matrix dimension N                               */
+  int64_t row_begin, row_end;   /* this rank's rows [row_begin, row_end)                    */
+  const int64_t* row_ptr;       /* row_end-row_begin+1 entries, row_ptr[0] == 0, non-decreasing */
+  const int64_t* col;           /* row_ptr[last] global column ids, in [0, n_global); any
+                                   order inside a row (that order is the summation order)   */
+  const double* val;            /* 2*row_ptr[last] doubles, interleaved (re, im)            */
+  int mem;                      /* KPM_MEM_HOST or KPM_MEM_DEVICE (all three arrays)        */
+} kpm_csr;
+
+/* Create a context on opt->device.  nranks > 1: also creates the NCCL communicator
+ * (collective).  *out is NULL on failure. */
+kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt);
+
+/* Store the Hermitian matrix H and the rescaling H~ = a(H - b 1), a > 0.
+ * Builds the SELL-C-sigma copy on the device and, for nranks > 1, the
+ * halo maps of the row distribution.  Hermiticity is not checked.  Replaces any previous
+ * matrix. */
+kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, double b);
+
+/* KPM-DOS moments with R random start vectors |rand()>: Z4 phases
+ * {1, i, -1, -i} from Philox4x32-10 keyed by (global row, global column, seed) (DESIGN.md
+ * R6), so the result does not depend on nranks or the SELL permutation.
+ *   M     number of moments, even, >= 2: M/2 sweeps = init + (M/2 - 1) aug_spmmv sweeps.
+ *   R     number of random vectors, >= 1 (processed in blocks of at most 32 columns).
+ *   mu    out, host, M doubles: mu_n = (1/R) sum_r Re m_n^(r) with m_0 = eta_0, m_1 = eta_1,
+ *         m_2k = 2 eta_2k - m_0, m_2k+1 = 2 eta_2k+1 - m_1; E[mu_n] = tr T_n(H~).
+ *         Identical on all ranks.
+ *   eta   out, optional (NULL), host, 2*R*M doubles: eta_n of column r at [(r*M + n)*2 + {re,im}].
+ * Returns KPM_WDIVERGED (after writing mu/eta) if |mu_n| > mu_0 (1 + 1e-8) for some n. */
+kpm_status kpm_moments(kpm_ctx* ctx, int M, int R, uint64_t seed, double* mu, double* eta);
+
+/* Same with explicit start vectors: v0 = host, (row_end-row_begin) x R row-major complex
+ * block of this rank's rows (2*n_loc*R doubles).  mu uses the same formula (not normalised
+ * by eta_0).  KPM_EZERONORM if a column has eta_0 == 0 (mu/eta still written). */
+kpm_status kpm_moments_v0(kpm_ctx* ctx, int M, int R, const double* v0, double* mu, double* eta);
+
+/* Device time of the last kpm_moments* call, measured with CUDA events on the context's
+ * stream: total_ms = start-vector init .. last eta reduction; sweep_ms = average duration
+ * of one main aug_spmmv sweep (the hot kernel); n_sweeps = main sweeps timed. */
+kpm_status kpm_last_timing(const kpm_ctx* ctx, double* total_ms, double* sweep_ms, int* n_sweeps);
+
+/* Sizes of the SELL copy, for kpm_export_sell.  n_chunks*C = n_pad. */
+typedef struct {
+  int64_t n_loc;     /* local rows                                       */
+  int64_t n_pad;     /* n_chunks * C                                     */
+  int64_t n_chunks;
+  int64_t n_slots;   /* cptr[n_chunks]: stored entries including padding */
+  int64_t n_halo;    /* halo rows appended after n_pad                   */
+  int C, sigma;
+} kpm_sell_info;
+
+kpm_status kpm_get_sell_info(const kpm_ctx* ctx, kpm_sell_info* info);
+
+/* Copy the SELL arrays to host buffers sized from kpm_sell_info:
+ * val 2*n_slots doubles, col n_slots int32, cptr n_chunks+1 int64, perm n_loc int32
+ * (perm[p] = local row stored at position p), halo n_halo int64 (global column of each
+ * halo slot).  Any pointer may be NULL to skip that array. */
+kpm_status kpm_export_sell(const kpm_ctx* ctx, double* val, int32_t* col, int64_t* cptr,
+                           int32_t* perm, int64_t* halo);
+
+/* Human-readable description of the last error on ctx (or of the last kpm_create failure
+ * when ctx is NULL).  Valid until the next call on ctx. */
+const char* kpm_last_error(const kpm_ctx* ctx);
+
+/* Release everything.  NULL-safe. */
+void kpm_destroy(kpm_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KPM_H */

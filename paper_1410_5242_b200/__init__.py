@@ -1,0 +1,181 @@
+"""B200-native KPM-DOS hot path (arXiv:1410.5242): thin Python binding of libkpm.so.
+
+Argument marshalling only -- every step of the path runs in the library's sm_100a kernels
+(include/kpm.h documents the ABI).  There is no CPU fallback: importing the binding
+without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libkpm.so")
+
+KPM_OK, KPM_EINVAL, KPM_ESTATE, KPM_ERANGE, KPM_ENOMEM, KPM_ECUDA, KPM_ENCCL, KPM_EZERONORM, KPM_WDIVERGED = range(9)
+KPM_MEM_HOST, KPM_MEM_DEVICE = 0, 1
+STATUS_NAMES = ["KPM_OK", "KPM_EINVAL", "KPM_ESTATE", "KPM_ERANGE", "KPM_ENOMEM", "KPM_ECUDA", "KPM_ENCCL",
+                "KPM_EZERONORM", "KPM_WDIVERGED"]
+
+# exported symbols declared in include/kpm.h
+ABI_SYMBOLS = ["kpm_create", "kpm_set_matrix", "kpm_moments", "kpm_moments_v0", "kpm_last_timing",
+               "kpm_get_sell_info", "kpm_export_sell", "kpm_last_error", "kpm_destroy"]
+
+
+class KpmError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else status}: {msg}")
+        self.status = status
+
+
+class kpm_options(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("nranks", ctypes.c_int), ("rank", ctypes.c_int),
+                ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p), ("sell_C", ctypes.c_int),
+                ("sell_sigma", ctypes.c_int), ("flags", ctypes.c_uint)]
+
+
+class kpm_csr(ctypes.Structure):
+    _fields_ = [("n_global", ctypes.c_int64), ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64),
+                ("row_ptr", ctypes.c_void_p), ("col", ctypes.c_void_p), ("val", ctypes.c_void_p),
+                ("mem", ctypes.c_int)]
+
+
+class kpm_sell_info(ctypes.Structure):
+    _fields_ = [("n_loc", ctypes.c_int64), ("n_pad", ctypes.c_int64), ("n_chunks", ctypes.c_int64),
+                ("n_slots", ctypes.c_int64), ("n_halo", ctypes.c_int64), ("C", ctypes.c_int),
+                ("sigma", ctypes.c_int)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load the in-tree libkpm.so (raises if it is missing: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, u64, dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+    lib.kpm_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(kpm_options)]
+    lib.kpm_set_matrix.argtypes = [P, ctypes.POINTER(kpm_csr), dbl, dbl]
+    lib.kpm_moments.argtypes = [P, i32, i32, u64, P, P]
+    lib.kpm_moments_v0.argtypes = [P, i32, i32, P, P, P]
+    lib.kpm_last_timing.argtypes = [P, P, P, P]
+    lib.kpm_get_sell_info.argtypes = [P, ctypes.POINTER(kpm_sell_info)]
+    lib.kpm_export_sell.argtypes = [P, P, P, P, P, P]
+    lib.kpm_last_error.argtypes = [P]
+    lib.kpm_last_error.restype = ctypes.c_char_p
+    lib.kpm_destroy.argtypes = [P]
+    lib.kpm_destroy.restype = None
+    for name in ABI_SYMBOLS:
+        if name not in ("kpm_last_error", "kpm_destroy"):
+            getattr(lib, name).restype = i32
+    _lib = lib
+    return lib
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(ctypes.c_void_p)
+    return ctypes.c_void_p(int(a.data_ptr()))  # torch tensor (device memory plumbing)
+
+
+class KpmContext:
+    """One rank's context (kpm_create ... kpm_destroy)."""
+
+    def __init__(self, device=0, nranks=1, rank=0, nccl_unique_id=None, cuda_stream=None, sell_C=32, sell_sigma=1):
+        self.lib = load_library()
+        self._uid = None if nccl_unique_id is None else ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
+        opt = kpm_options(device, nranks, rank, ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None,
+                          cuda_stream, sell_C, sell_sigma, 0)
+        h = ctypes.c_void_p()
+        st = self.lib.kpm_create(ctypes.byref(h), ctypes.byref(opt))
+        if st != KPM_OK:
+            raise KpmError(st, self.lib.kpm_last_error(None).decode())
+        self.h = h
+        self.last_status = KPM_OK
+
+    def _check(self, st, allow=()):
+        self.last_status = st
+        if st != KPM_OK and st not in allow:
+            raise KpmError(st, self.lib.kpm_last_error(self.h).decode())
+        return st
+
+    def set_matrix(self, row_ptr, col, val, a, b, n_global=None, row_begin=0, mem=KPM_MEM_HOST):
+        """kpm_set_matrix from numpy (host) or torch (device) CSR arrays; val complex128 or
+        interleaved float64."""
+        keep = []
+        if mem == KPM_MEM_HOST:
+            row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+            col = np.ascontiguousarray(col, dtype=np.int64)
+            val = np.ascontiguousarray(val)
+            if val.dtype != np.complex128:
+                val = np.ascontiguousarray(val, dtype=np.float64)
+            keep = [row_ptr, col, val]
+        n_loc = len(row_ptr) - 1
+        if n_global is None:
+            n_global = row_begin + n_loc
+        csr = kpm_csr(n_global, row_begin, row_begin + n_loc, _ptr(row_ptr), _ptr(col), _ptr(val), mem)
+        self._check(self.lib.kpm_set_matrix(self.h, ctypes.byref(csr), float(a), float(b)))
+        del keep
+
+    def moments(self, M, R, seed, want_eta=True, allow_warning=True):
+        """(mu (M,), eta (R, M) complex or None)."""
+        mu = np.zeros(M)
+        eta = np.zeros((R, M), dtype=np.complex128) if want_eta else None
+        allow = (KPM_WDIVERGED,) if allow_warning else ()
+        self._check(self.lib.kpm_moments(self.h, M, R, seed, _ptr(mu), _ptr(eta)), allow)
+        return mu, eta
+
+    def moments_v0(self, M, v0, allow=(KPM_WDIVERGED,)):
+        v0 = np.ascontiguousarray(v0, dtype=np.complex128)
+        if v0.ndim == 1:
+            v0 = v0[:, None]
+        R = v0.shape[1]
+        mu = np.zeros(M)
+        eta = np.zeros((R, M), dtype=np.complex128)
+        self._check(self.lib.kpm_moments_v0(self.h, M, R, _ptr(v0), _ptr(mu), _ptr(eta)), allow)
+        return mu, eta
+
+    def last_timing(self):
+        t, s, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        self._check(self.lib.kpm_last_timing(self.h, ctypes.byref(t), ctypes.byref(s), ctypes.byref(n)))
+        return t.value, s.value, n.value
+
+    def sell_info(self):
+        info = kpm_sell_info()
+        self._check(self.lib.kpm_get_sell_info(self.h, ctypes.byref(info)))
+        return info
+
+    def export_sell(self):
+        info = self.sell_info()
+        val = np.zeros(info.n_slots, dtype=np.complex128)
+        col = np.zeros(info.n_slots, dtype=np.int32)
+        cptr = np.zeros(info.n_chunks + 1, dtype=np.int64)
+        perm = np.zeros(info.n_loc, dtype=np.int32)
+        halo = np.zeros(max(info.n_halo, 1), dtype=np.int64)
+        self._check(self.lib.kpm_export_sell(self.h, _ptr(val), _ptr(col), _ptr(cptr), _ptr(perm), _ptr(halo)))
+        return dict(val=val, col=col, cptr=cptr, perm=perm, halo=halo[: info.n_halo], n_pad=info.n_pad)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.kpm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

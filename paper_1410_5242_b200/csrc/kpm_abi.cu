@@ -1,0 +1,454 @@
+// C ABI of the B200 KPM-DOS hot path (include/kpm.h).  Host orchestration only: every step
+// of the path (start block, sweeps, dot products, reductions) runs in the kernels of
+// kernels.cu; this file validates arguments, builds the SELL copy, owns device memory and
+// enqueues the work on one stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kpm.h"
+#include "kpm_internal.h"
+#include "sell_build.h"
+
+using namespace kpm;
+
+struct kpm_ctx {
+  kpm_options opt{};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool sticky = false;
+  std::string err;
+  int num_sms = 148;
+  int segment = 1;       // chunk-schedule segment (tuning knob, env KPM_SEGMENT)
+  int grid_per_sm = 0;   // 0 -> occupancy (env KPM_GRID_PER_SM)
+
+  // matrix
+  bool have_matrix = false;
+  int64_t n_global = 0, row_begin = 0, row_end = 0;
+  double a = 0.0, b = 0.0;
+  DevSell sell;
+  std::vector<int64_t> halo;  // global ids of halo slots
+
+  // work buffers (grow-only)
+  double2* X0 = nullptr;
+  double2* X1 = nullptr;
+  size_t x_cap = 0;  // elements per buffer
+  double* partials = nullptr;
+  size_t partials_cap = 0;  // doubles
+  double2* eta_even = nullptr;
+  double2* eta_odd = nullptr;
+  size_t eta_cap = 0;  // double2 per array
+  double2* h_eta = nullptr;  // pinned staging, 2*eta_cap
+  double2* v0_dev = nullptr;
+  size_t v0_cap = 0;
+
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double last_total_ms = 0.0, last_sweep_ms = 0.0;
+  int last_n_sweeps = 0;
+};
+
+static std::string g_create_err;
+
+#define KPM_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                \
+      ctx->sticky = true;                                                           \
+      return KPM_ECUDA;                                                             \
+    }                                                                               \
+  } while (0)
+
+static kpm_status fail(kpm_ctx* ctx, kpm_status st, const std::string& msg) {
+  ctx->err = msg;
+  return st;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return s ? atoi(s) : dflt;
+}
+
+extern "C" kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt) {
+  if (!out) return KPM_EINVAL;
+  *out = nullptr;
+  if (!opt) {
+    g_create_err = "opt is NULL";
+    return KPM_EINVAL;
+  }
+  if (opt->nranks != 1 || opt->rank != 0) {
+    g_create_err = "nranks > 1 requires the NCCL build (not in this library yet)";
+    return KPM_EINVAL;
+  }
+  const int C = opt->sell_C ? opt->sell_C : kC;
+  const int sigma = opt->sell_sigma ? opt->sell_sigma : 1;
+  if (C != kC || sigma < 1 || (sigma > 1 && sigma % C != 0)) {
+    g_create_err = "unsupported SELL parameters (C must be 32, sigma 1 or a multiple of 32)";
+    return KPM_EINVAL;
+  }
+  kpm_ctx* ctx = new kpm_ctx();
+  ctx->opt = *opt;
+  ctx->opt.sell_C = C;
+  ctx->opt.sell_sigma = sigma;
+  cudaError_t e = cudaSetDevice(opt->device);
+  if (e == cudaSuccess && opt->cuda_stream) {
+    ctx->stream = (cudaStream_t)opt->cuda_stream;
+  } else if (e == cudaSuccess) {
+    e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    ctx->own_stream = (e == cudaSuccess);
+  }
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, opt->device);
+  for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev[i]);
+  if (e != cudaSuccess) {
+    g_create_err = std::string("CUDA: ") + cudaGetErrorString(e);
+    kpm_destroy(ctx);
+    return KPM_ECUDA;
+  }
+  ctx->segment = std::max(1, env_int("KPM_SEGMENT", 1));
+  ctx->grid_per_sm = std::max(0, env_int("KPM_GRID_PER_SM", 0));
+  *out = ctx;
+  return KPM_OK;
+}
+
+extern "C" void kpm_destroy(kpm_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->opt.device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->sell.val);
+  cudaFree(ctx->sell.col);
+  cudaFree(ctx->sell.cptr);
+  cudaFree(ctx->sell.perm);
+  cudaFree(ctx->X0);
+  cudaFree(ctx->X1);
+  cudaFree(ctx->partials);
+  cudaFree(ctx->eta_even);
+  cudaFree(ctx->eta_odd);
+  cudaFree(ctx->v0_dev);
+  if (ctx->h_eta) cudaFreeHost(ctx->h_eta);
+  for (int i = 0; i < 4; ++i)
+    if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+extern "C" const char* kpm_last_error(const kpm_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+static void free_sell(DevSell& s) {
+  cudaFree(s.val);
+  cudaFree(s.col);
+  cudaFree(s.cptr);
+  cudaFree(s.perm);
+  s = DevSell();
+}
+
+extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, double b) {
+  if (!ctx) return KPM_EINVAL;
+  if (ctx->sticky) return fail(ctx, KPM_ESTATE, "context has a sticky CUDA/NCCL error: " + ctx->err);
+  if (!H || !H->row_ptr || !H->col || !H->val) return fail(ctx, KPM_EINVAL, "NULL matrix pointer");
+  if (!(a > 0.0) || !std::isfinite(a) || !std::isfinite(b)) return fail(ctx, KPM_EINVAL, "need finite a > 0 and finite b");
+  if (H->mem != KPM_MEM_HOST && H->mem != KPM_MEM_DEVICE) return fail(ctx, KPM_EINVAL, "bad mem kind");
+  const int64_t n_loc = H->row_end - H->row_begin;
+  if (H->n_global < 1 || H->row_begin < 0 || n_loc < 1 || H->row_end > H->n_global)
+    return fail(ctx, KPM_EINVAL, "bad row range");
+  if (ctx->opt.nranks == 1 && (H->row_begin != 0 || H->row_end != H->n_global))
+    return fail(ctx, KPM_EINVAL, "single rank must own all rows");
+  KPM_CUDA(cudaSetDevice(ctx->opt.device));
+
+  // host views of the CSR (device input is staged through the host for the build)
+  std::vector<int64_t> rp_h, col_h;
+  std::vector<double> val_h;
+  const int64_t* rp = H->row_ptr;
+  const int64_t* col = H->col;
+  const double* val = H->val;
+  if (H->mem == KPM_MEM_DEVICE) {
+    rp_h.resize(n_loc + 1);
+    KPM_CUDA(cudaMemcpy(rp_h.data(), H->row_ptr, sizeof(int64_t) * (n_loc + 1), cudaMemcpyDeviceToHost));
+    const int64_t nnz = rp_h[n_loc];
+    if (nnz < 0) return fail(ctx, KPM_EINVAL, "malformed row_ptr");
+    col_h.resize(nnz);
+    val_h.resize(2 * nnz);
+    KPM_CUDA(cudaMemcpy(col_h.data(), H->col, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
+    KPM_CUDA(cudaMemcpy(val_h.data(), H->val, sizeof(double) * 2 * nnz, cudaMemcpyDeviceToHost));
+    rp = rp_h.data();
+    col = col_h.data();
+    val = val_h.data();
+  }
+  if (rp[0] != 0) return fail(ctx, KPM_EINVAL, "row_ptr[0] != 0");
+  for (int64_t i = 0; i < n_loc; ++i)
+    if (rp[i + 1] < rp[i]) return fail(ctx, KPM_EINVAL, "row_ptr not non-decreasing");
+  const int64_t nnz = rp[n_loc];
+  for (int64_t k = 0; k < nnz; ++k) {
+    if (col[k] < 0 || col[k] >= H->n_global) return fail(ctx, KPM_ERANGE, "column outside [0, n_global)");
+    if (!std::isfinite(val[2 * k]) || !std::isfinite(val[2 * k + 1])) return fail(ctx, KPM_EINVAL, "non-finite value");
+  }
+
+  HostSell hs;
+  std::string berr;
+  int st = build_sell_host(rp, col, val, n_loc, H->row_begin, H->row_end, ctx->opt.sell_C, ctx->opt.sell_sigma, hs,
+                           berr);
+  if (st) return fail(ctx, (kpm_status)st, berr);
+  if (ctx->opt.nranks == 1 && hs.n_halo != 0) return fail(ctx, KPM_EINVAL, "internal: halo on a single rank");
+
+  // upload
+  free_sell(ctx->sell);
+  ctx->have_matrix = false;
+  DevSell& d = ctx->sell;
+  d.n_loc = hs.n_loc;
+  d.n_pad = hs.n_pad;
+  d.n_chunks = hs.n_chunks;
+  d.n_slots = hs.cptr[hs.n_chunks];
+  d.n_halo = hs.n_halo;
+  auto alloc = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
+  cudaError_t e = alloc((void**)&d.val, sizeof(double2) * d.n_slots);
+  if (e == cudaSuccess) e = alloc((void**)&d.col, sizeof(int) * d.n_slots);
+  if (e == cudaSuccess) e = alloc((void**)&d.cptr, sizeof(int64_t) * (d.n_chunks + 1));
+  if (e == cudaSuccess) e = alloc((void**)&d.perm, sizeof(int) * d.n_loc);
+  if (e != cudaSuccess) {
+    free_sell(ctx->sell);
+    cudaGetLastError();
+    return fail(ctx, KPM_ENOMEM, std::string("device allocation for the matrix failed: ") + cudaGetErrorString(e));
+  }
+  KPM_CUDA(cudaMemcpy(d.val, hs.val.data(), sizeof(double2) * d.n_slots, cudaMemcpyHostToDevice));
+  KPM_CUDA(cudaMemcpy(d.col, hs.col.data(), sizeof(int) * d.n_slots, cudaMemcpyHostToDevice));
+  KPM_CUDA(cudaMemcpy(d.cptr, hs.cptr.data(), sizeof(int64_t) * (d.n_chunks + 1), cudaMemcpyHostToDevice));
+  KPM_CUDA(cudaMemcpy(d.perm, hs.perm.data(), sizeof(int) * d.n_loc, cudaMemcpyHostToDevice));
+  ctx->halo = hs.halo;
+  ctx->n_global = H->n_global;
+  ctx->row_begin = H->row_begin;
+  ctx->row_end = H->row_end;
+  ctx->a = a;
+  ctx->b = b;
+  ctx->have_matrix = true;
+  return KPM_OK;
+}
+
+static int block_width(int r) {
+  int w = 1;
+  while (w < r) w <<= 1;
+  return w;
+}
+
+static kpm_status ensure(kpm_ctx* ctx, void** p, size_t* cap, size_t need, size_t elsize) {
+  if (*cap >= need) return KPM_OK;
+  cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  cudaError_t e = cudaMalloc(p, need * elsize);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, KPM_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
+  }
+  *cap = need;
+  return KPM_OK;
+}
+
+// One block of up to 32 columns: start block, M/2 sweeps, eta reduction, D2H.
+// eta_cols: host, [(r*M + n)] double2 for the rb columns of this block.
+static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint64_t seed, const double* v0,
+                            double2* eta_cols, bool first, bool last) {
+  const int Rk = block_width(rb);
+  const int n_sweeps = M / 2;
+  const DevSell& s = ctx->sell;
+  const int64_t n_rows_total = s.n_pad + s.n_halo;
+  kpm_status st;
+  size_t xcap = ctx->x_cap;
+  if ((st = ensure(ctx, (void**)&ctx->X0, &xcap, (size_t)n_rows_total * Rk, sizeof(double2))) != KPM_OK) return st;
+  xcap = ctx->x_cap;
+  if ((st = ensure(ctx, (void**)&ctx->X1, &xcap, (size_t)n_rows_total * Rk, sizeof(double2))) != KPM_OK) return st;
+  ctx->x_cap = xcap;
+
+  const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, sweep_occupancy(Rk, false));
+  const int rpg = rows_per_group(Rk);
+  const int64_t n_groups = s.n_pad / rpg;
+  const int64_t n_segs = (n_groups + 8LL * ctx->segment - 1) / (8LL * ctx->segment);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * occ, n_segs));
+  const size_t per_sweep = (size_t)3 * Rk * grid;
+  if ((st = ensure(ctx, (void**)&ctx->partials, &ctx->partials_cap, per_sweep * n_sweeps, sizeof(double))) != KPM_OK)
+    return st;
+  size_t ecap = ctx->eta_cap;
+  if ((st = ensure(ctx, (void**)&ctx->eta_even, &ecap, (size_t)n_sweeps * kMaxBlockWidth, sizeof(double2))) != KPM_OK)
+    return st;
+  ecap = ctx->eta_cap;
+  if ((st = ensure(ctx, (void**)&ctx->eta_odd, &ecap, (size_t)n_sweeps * kMaxBlockWidth, sizeof(double2))) != KPM_OK)
+    return st;
+  if (ecap > ctx->eta_cap || !ctx->h_eta) {
+    if (ctx->h_eta) cudaFreeHost(ctx->h_eta);
+    ctx->h_eta = nullptr;
+    if (cudaMallocHost((void**)&ctx->h_eta, sizeof(double2) * 2 * ecap) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, KPM_ENOMEM, "pinned host allocation failed");
+    }
+  }
+  ctx->eta_cap = ecap;
+
+  cudaStream_t str = ctx->stream;
+  if (first) KPM_CUDA(cudaEventRecord(ctx->ev[0], str));
+  // a1: start block
+  if (v0) {
+    size_t vcap = ctx->v0_cap;
+    if ((st = ensure(ctx, (void**)&ctx->v0_dev, &vcap, (size_t)s.n_loc * rb, sizeof(double2))) != KPM_OK) return st;
+    ctx->v0_cap = vcap;
+    KPM_CUDA(cudaMemcpyAsync(ctx->v0_dev, v0, sizeof(double2) * s.n_loc * rb, cudaMemcpyHostToDevice, str));
+    KPM_CUDA(launch_v0_upload_permute(ctx->X0, ctx->X1, ctx->v0_dev, s.perm, s.n_loc, n_rows_total, Rk, rb, str));
+  } else {
+    KPM_CUDA(launch_z4_init(ctx->X0, ctx->X1, s.perm, s.n_loc, n_rows_total, Rk, ctx->row_begin, col_begin, rb, seed,
+                            str));
+  }
+  SweepArgs sa;
+  sa.val = s.val;
+  sa.col = s.col;
+  sa.cptr = s.cptr;
+  sa.n_loc = s.n_loc;
+  sa.group_begin = 0;
+  sa.group_end = n_groups;
+  sa.segment = ctx->segment;
+  sa.b = ctx->b;
+  // a2: init sweep  W = a(H - b)V, eta_0, eta_1
+  sa.V = ctx->X0;
+  sa.W = ctx->X1;
+  sa.scale = ctx->a;
+  sa.partials = ctx->partials;
+  KPM_CUDA(launch_aug_spmmv(Rk, true, sa, grid, str));
+  // a3: main sweeps  W <- 2a(H - b)V - W, eta_2m, eta_2m+1
+  KPM_CUDA(cudaEventRecord(ctx->ev[1], str));
+  sa.scale = 2.0 * ctx->a;
+  for (int m = 1; m < n_sweeps; ++m) {
+    sa.V = (m & 1) ? ctx->X1 : ctx->X0;
+    sa.W = (m & 1) ? ctx->X0 : ctx->X1;
+    sa.partials = ctx->partials + per_sweep * m;
+    KPM_CUDA(launch_aug_spmmv(Rk, false, sa, grid, str));
+  }
+  KPM_CUDA(cudaEventRecord(ctx->ev[2], str));
+  // a4: deterministic grid reduction of all sweeps' partials
+  KPM_CUDA(launch_eta_finalize(ctx->partials, n_sweeps, Rk, grid, ctx->eta_even, ctx->eta_odd, str));
+  KPM_CUDA(cudaMemcpyAsync(ctx->h_eta, ctx->eta_even, sizeof(double2) * n_sweeps * Rk, cudaMemcpyDeviceToHost, str));
+  KPM_CUDA(cudaMemcpyAsync(ctx->h_eta + ctx->eta_cap, ctx->eta_odd, sizeof(double2) * n_sweeps * Rk,
+                           cudaMemcpyDeviceToHost, str));
+  if (last) KPM_CUDA(cudaEventRecord(ctx->ev[3], str));
+  KPM_CUDA(cudaStreamSynchronize(str));
+  for (int r = 0; r < rb; ++r)
+    for (int m = 0; m < n_sweeps; ++m) {
+      eta_cols[(size_t)r * M + 2 * m] = ctx->h_eta[(size_t)m * Rk + r];
+      eta_cols[(size_t)r * M + 2 * m + 1] = ctx->h_eta[ctx->eta_cap + (size_t)m * Rk + r];
+    }
+  float ms = 0.f;
+  if (n_sweeps > 1) {
+    KPM_CUDA(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]));
+    ctx->last_sweep_ms = ms / (n_sweeps - 1);
+    ctx->last_n_sweeps = n_sweeps - 1;
+  } else {
+    ctx->last_sweep_ms = 0.0;
+    ctx->last_n_sweeps = 0;
+  }
+  if (last) {
+    KPM_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]));
+    ctx->last_total_ms = ms;
+  }
+  return KPM_OK;
+}
+
+static kpm_status moments_common(kpm_ctx* ctx, int M, int R, uint64_t seed, const double* v0, double* mu,
+                                 double* eta) {
+  if (!ctx) return KPM_EINVAL;
+  if (ctx->sticky) return fail(ctx, KPM_ESTATE, "context has a sticky CUDA/NCCL error: " + ctx->err);
+  if (!ctx->have_matrix) return fail(ctx, KPM_ESTATE, "kpm_set_matrix has not been called");
+  if (M < 2 || (M % 2) != 0) return fail(ctx, KPM_EINVAL, "M must be even and >= 2");
+  if (R < 1) return fail(ctx, KPM_EINVAL, "R must be >= 1");
+  if (!mu) return fail(ctx, KPM_EINVAL, "mu is NULL");
+  KPM_CUDA(cudaSetDevice(ctx->opt.device));
+  std::vector<double2> eta_all((size_t)R * M);
+  const int64_t n_loc = ctx->sell.n_loc;
+  std::vector<double> v0_block;
+  for (int c0 = 0; c0 < R; c0 += kMaxBlockWidth) {
+    const int rb = std::min(kMaxBlockWidth, R - c0);
+    const double* v0b = nullptr;
+    if (v0) {  // columns c0..c0+rb-1 of the caller's n_loc x R block, repacked n_loc x rb
+      v0_block.resize((size_t)2 * n_loc * rb);
+      for (int64_t i = 0; i < n_loc; ++i)
+        for (int r = 0; r < rb; ++r) {
+          v0_block[2 * (i * rb + r)] = v0[2 * (i * R + c0 + r)];
+          v0_block[2 * (i * rb + r) + 1] = v0[2 * (i * R + c0 + r) + 1];
+        }
+      v0b = v0_block.data();
+    }
+    kpm_status st = run_block(ctx, M, rb, c0, seed, v0b, eta_all.data() + (size_t)c0 * M, c0 == 0,
+                              c0 + kMaxBlockWidth >= R);
+    if (st != KPM_OK) return st;
+  }
+  // a6: eta -> mu (doubling identities, stochastic trace)
+  bool zero_norm = false;
+  std::vector<double> acc(M, 0.0);
+  std::vector<double2> m(M);
+  for (int r = 0; r < R; ++r) {
+    const double2* e = eta_all.data() + (size_t)r * M;
+    if (e[0].x == 0.0) zero_norm = true;
+    m[0] = e[0];
+    m[1] = e[1];
+    for (int k = 1; 2 * k < M; ++k) {
+      m[2 * k] = make_double2(2.0 * e[2 * k].x - m[0].x, 2.0 * e[2 * k].y - m[0].y);
+      m[2 * k + 1] = make_double2(2.0 * e[2 * k + 1].x - m[1].x, 2.0 * e[2 * k + 1].y - m[1].y);
+    }
+    for (int n = 0; n < M; ++n) acc[n] += m[n].x;
+  }
+  bool diverged = false;
+  for (int n = 0; n < M; ++n) mu[n] = acc[n] / (double)R;
+  for (int n = 1; n < M; ++n)
+    if (!(std::fabs(mu[n]) <= std::fabs(mu[0]) * (1.0 + 1e-8))) diverged = true;
+  if (eta) std::memcpy(eta, eta_all.data(), sizeof(double2) * (size_t)R * M);
+  if (v0 && zero_norm) return fail(ctx, KPM_EZERONORM, "a start column has eta_0 = 0");
+  if (diverged) return fail(ctx, KPM_WDIVERGED, "|mu_n| > mu_0: a, b do not map the spectrum into [-1, 1]");
+  return KPM_OK;
+}
+
+extern "C" kpm_status kpm_moments(kpm_ctx* ctx, int M, int R, uint64_t seed, double* mu, double* eta) {
+  return moments_common(ctx, M, R, seed, nullptr, mu, eta);
+}
+
+extern "C" kpm_status kpm_moments_v0(kpm_ctx* ctx, int M, int R, const double* v0, double* mu, double* eta) {
+  if (ctx && !v0) return fail(ctx, KPM_EINVAL, "v0 is NULL");
+  return moments_common(ctx, M, R, 0, v0, mu, eta);
+}
+
+extern "C" kpm_status kpm_last_timing(const kpm_ctx* ctx, double* total_ms, double* sweep_ms, int* n_sweeps) {
+  if (!ctx) return KPM_EINVAL;
+  if (total_ms) *total_ms = ctx->last_total_ms;
+  if (sweep_ms) *sweep_ms = ctx->last_sweep_ms;
+  if (n_sweeps) *n_sweeps = ctx->last_n_sweeps;
+  return KPM_OK;
+}
+
+extern "C" kpm_status kpm_get_sell_info(const kpm_ctx* ctx, kpm_sell_info* info) {
+  if (!ctx || !info) return KPM_EINVAL;
+  if (!ctx->have_matrix) return KPM_ESTATE;
+  info->n_loc = ctx->sell.n_loc;
+  info->n_pad = ctx->sell.n_pad;
+  info->n_chunks = ctx->sell.n_chunks;
+  info->n_slots = ctx->sell.n_slots;
+  info->n_halo = ctx->sell.n_halo;
+  info->C = ctx->opt.sell_C;
+  info->sigma = ctx->opt.sell_sigma;
+  return KPM_OK;
+}
+
+extern "C" kpm_status kpm_export_sell(const kpm_ctx* ctx_c, double* val, int32_t* col, int64_t* cptr, int32_t* perm,
+                                      int64_t* halo) {
+  kpm_ctx* ctx = const_cast<kpm_ctx*>(ctx_c);
+  if (!ctx) return KPM_EINVAL;
+  if (!ctx->have_matrix) return fail(ctx, KPM_ESTATE, "no matrix");
+  KPM_CUDA(cudaSetDevice(ctx->opt.device));
+  const DevSell& s = ctx->sell;
+  if (val) KPM_CUDA(cudaMemcpy(val, s.val, sizeof(double2) * s.n_slots, cudaMemcpyDeviceToHost));
+  if (col) KPM_CUDA(cudaMemcpy(col, s.col, sizeof(int) * s.n_slots, cudaMemcpyDeviceToHost));
+  if (cptr) KPM_CUDA(cudaMemcpy(cptr, s.cptr, sizeof(int64_t) * (s.n_chunks + 1), cudaMemcpyDeviceToHost));
+  if (perm) KPM_CUDA(cudaMemcpy(perm, s.perm, sizeof(int) * s.n_loc, cudaMemcpyDeviceToHost));
+  if (halo && !ctx->halo.empty()) std::memcpy(halo, ctx->halo.data(), sizeof(int64_t) * ctx->halo.size());
+  return KPM_OK;
+}

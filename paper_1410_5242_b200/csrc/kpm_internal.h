@@ -1,0 +1,54 @@
+// Internal declarations of the B200 KPM library (not part of the ABI; see include/kpm.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace kpm {
+
+constexpr int kC = 32;             // SELL chunk height = warpSize (north_star subsystem 1)
+constexpr int kThreads = 256;      // threads per CTA of the sweep kernels (8 warps)
+constexpr int kMaxBlockWidth = 32; // widest specialised block (R per batch)
+
+// Device-side SELL-C-sigma matrix ("Data layout in HBM").
+struct DevSell {
+  double2* val = nullptr;  // n_slots, chunk-column-major: entry j of row k of chunk c at cptr[c]+j*32+k
+  int* col = nullptr;      // n_slots, int32 local column (position in the local+halo vector)
+  int64_t* cptr = nullptr; // n_chunks+1
+  int* perm = nullptr;     // n_loc: local row stored at position p
+  int64_t n_loc = 0, n_pad = 0, n_chunks = 0, n_slots = 0, n_halo = 0;
+};
+
+// One aug_spmmv sweep over the row groups [group_begin, group_end).
+struct SweepArgs {
+  const double2* val;
+  const int* col;
+  const int64_t* cptr;
+  const double2* V;    // nu_m   (read only)
+  double2* W;          // nu_{m-1} in, nu_{m+1} out
+  int64_t n_loc;
+  int64_t group_begin, group_end;
+  int segment;         // consecutive 8-group steps a CTA takes before jumping (chunk schedule)
+  double scale;        // 2a for the main sweep, a for the init sweep
+  double b;
+  double* partials;    // [3R][gridDim]: per-CTA (eta_even, Re eta_odd, Im eta_odd) of this sweep
+};
+
+// Launch helpers (kernels.cu).  All return cudaGetLastError() of the launch.
+cudaError_t launch_z4_init(double2* V, double2* W, const int* perm, int64_t n_loc, int64_t n_rows_total,
+                           int R, int64_t row_begin, int64_t col_begin, int r_valid, uint64_t seed,
+                           cudaStream_t s);
+cudaError_t launch_v0_upload_permute(double2* V, double2* W, const double2* v0_dev, const int* perm,
+                                     int64_t n_loc, int64_t n_rows_total, int R, int r_valid,
+                                     cudaStream_t s);
+cudaError_t launch_aug_spmmv(int R, bool init, const SweepArgs& a, int grid, cudaStream_t s);
+int rows_per_group(int R);
+int sweep_occupancy(int R, bool init);
+// eta[m][r] (double2) for m in [0, n_sweeps) from partials[m][3R][grid]
+cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int grid, double2* eta_even,
+                                double2* eta_odd, cudaStream_t s);
+
+}  // namespace kpm

@@ -1,0 +1,92 @@
+// Host-side SELL-C-sigma builder and row-distribution halo list.
+//
+// SELL-C-sigma: Kreutzer et al., cited at PAPER.md P:126-128; C = 32 = warpSize; sigma-window
+// descending-length sort; "the CRS format (similar to SELL-1) can be used".
+// Layout contract: DESIGN.md "SELL-C-sigma" (the tests compare this builder bit for bit
+// with the independent numpy reference in oracle/sell_ref.py).
+#include "sell_build.h"
+
+#include <algorithm>
+#include <numeric>
+#include <stdexcept>
+
+namespace kpm {
+
+int build_sell_host(const int64_t* row_ptr, const int64_t* col, const double* val, int64_t n_loc,
+                    int64_t row_begin, int64_t row_end, int C, int sigma, HostSell& out, std::string& err) {
+  out = HostSell();
+  out.n_loc = n_loc;
+  out.C = C;
+  out.sigma = sigma;
+  std::vector<int64_t> len(n_loc);
+  for (int64_t i = 0; i < n_loc; ++i) len[i] = row_ptr[i + 1] - row_ptr[i];
+
+  // sigma-window stable sort by descending row length
+  out.perm.resize(n_loc);
+  std::iota(out.perm.begin(), out.perm.end(), 0);
+  if (sigma > 1) {
+    for (int64_t w0 = 0; w0 < n_loc; w0 += sigma) {
+      const int64_t w1 = std::min<int64_t>(w0 + sigma, n_loc);
+      std::stable_sort(out.perm.begin() + w0, out.perm.begin() + w1,
+                       [&](int a, int b) { return len[a] > len[b]; });
+    }
+  }
+  std::vector<int64_t> invperm(n_loc);
+  for (int64_t p = 0; p < n_loc; ++p) invperm[out.perm[p]] = p;
+
+  out.n_chunks = (n_loc + C - 1) / C;
+  out.n_pad = out.n_chunks * C;
+
+  // halo: distinct remote columns, ascending global id (== by owner rank, then id)
+  std::vector<int64_t>& halo = out.halo;
+  for (int64_t k = 0; k < row_ptr[n_loc]; ++k)
+    if (col[k] < row_begin || col[k] >= row_end) halo.push_back(col[k]);
+  std::sort(halo.begin(), halo.end());
+  halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+  out.n_halo = (int64_t)halo.size();
+  if (out.n_pad + out.n_halo > (int64_t)INT32_MAX) {
+    err = "local rows + halo rows exceed the int32 kernel index range";
+    return 3;
+  }
+
+  out.cptr.assign(out.n_chunks + 1, 0);
+  for (int64_t c = 0; c < out.n_chunks; ++c) {
+    int64_t m = 0;
+    for (int64_t k = 0; k < C; ++k) {
+      const int64_t p = c * C + k;
+      if (p < n_loc) m = std::max(m, len[out.perm[p]]);
+    }
+    out.cptr[c + 1] = out.cptr[c] + C * m;
+  }
+  const int64_t n_slots = out.cptr[out.n_chunks];
+  out.val.assign(2 * n_slots, 0.0);
+  out.col.resize(n_slots);
+  for (int64_t c = 0; c < out.n_chunks; ++c) {
+    const int64_t L = (out.cptr[c + 1] - out.cptr[c]) / C;
+    for (int64_t k = 0; k < C; ++k) {
+      const int64_t p = c * C + k;
+      const int64_t nrow = (p < n_loc) ? len[out.perm[p]] : 0;
+      const int64_t src = (p < n_loc) ? row_ptr[out.perm[p]] : 0;
+      for (int64_t j = 0; j < L; ++j) {
+        const int64_t d = out.cptr[c] + j * C + k;
+        if (j < nrow) {
+          const int64_t g = col[src + j];
+          int64_t lc;
+          if (g >= row_begin && g < row_end) {
+            lc = invperm[g - row_begin];
+          } else {
+            lc = out.n_pad + (std::lower_bound(halo.begin(), halo.end(), g) - halo.begin());
+          }
+          out.col[d] = (int32_t)lc;
+          out.val[2 * d] = val[2 * (src + j)];
+          out.val[2 * d + 1] = val[2 * (src + j) + 1];
+        } else {
+          out.col[d] = (int32_t)p;  // padding: value 0, column = own position
+        }
+      }
+    }
+  }
+  return 0;
+}
+
+}  // namespace kpm

@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle, element by element on the
+same seeded inputs (north_star gate: max_n |mu_gpu - mu_oracle| / mu_0 <= 1e-10, and per
+column max_n |eta_gpu - eta_oracle| / eta_0 <= 1e-10)."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import sell_ref
+from workloads.ti_lattice import (SEED, ZERO_POTENTIAL, Lattice, bloch_energies, gershgorin, generate_csr,
+                                  scale_factors)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1410_5242_b200 import build
+
+    build.build()
+    import paper_1410_5242_b200 as p
+
+    return p
+
+
+def problem(dims, potential=None, periodic_z=False):
+    lat = Lattice(*dims, periodic_z=periodic_z) if potential is None else Lattice(*dims, potential=potential,
+                                                                                  periodic_z=periodic_z)
+    rp, col, val = generate_csr(lat)
+    a, b = scale_factors(*gershgorin(rp, col, val))
+    return lat, rp, col, val, a, b
+
+
+def check(eta_g, mu_g, eta_o, cols=None):
+    if cols is not None:
+        eta_g = eta_g[cols]
+    eta0 = eta_o[:, :1].real
+    col_err = np.max(np.abs(eta_g - eta_o) / eta0)
+    assert col_err <= TOL, col_err
+    if cols is None:
+        mu_o, _ = oracle.eta_to_mu(eta_o)
+        assert np.max(np.abs(mu_g - mu_o)) / mu_o[0] <= TOL
+    return col_err
+
+
+@pytest.mark.parametrize("R", [1, 2, 4, 8, 16, 32])
+def test_c1_all_widths(pkg, R):
+    lat, rp, col, val, a, b = problem((8, 8, 8))
+    M = 64
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments(M, R, SEED)
+    eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, SEED)
+    check(eta, mu, eta_o)
+    assert mu[0] == lat.n  # Z4 vectors: eta_0 = N exactly
+
+
+@pytest.mark.parametrize("R", [3, 5, 33, 40])
+def test_ragged_widths_and_batches(pkg, R):
+    """Non-power-of-two widths pad to the next kernel width; R > 32 runs in blocks of 32
+    whose Philox columns continue the global column numbering."""
+    lat, rp, col, val, a, b = problem((6, 5, 7))  # N = 840: ragged last chunk (840 = 26*32 + 8)
+    M = 40
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments(M, R, SEED + 1)
+    eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, SEED + 1)
+    check(eta, mu, eta_o)
+
+
+@pytest.mark.parametrize("sigma", [1, 64])
+def test_zero_potential_and_sigma(pkg, sigma):
+    lat, rp, col, val, a, b = problem((5, 4, 9), potential=ZERO_POTENTIAL)
+    M, R = 100, 8
+    with pkg.KpmContext(sell_sigma=sigma) as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments(M, R, 77)
+        s = ctx.export_sell()
+    eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, 77)
+    check(eta, mu, eta_o)
+    ref = sell_ref.build_sell(rp, col, val, C=32, sigma=sigma)
+    assert np.array_equal(s["cptr"], ref["cptr"])
+    assert np.array_equal(s["col"], ref["col"])
+    assert np.array_equal(s["val"], ref["val"])
+    assert np.array_equal(s["perm"], ref["perm"])
+
+
+def test_sell_bit_exact_c1(pkg):
+    lat, rp, col, val, a, b = problem((8, 8, 8))
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        s = ctx.export_sell()
+    ref = sell_ref.build_sell(rp, col, val)
+    for k in ("cptr", "col", "val", "perm"):
+        assert np.array_equal(s[k], ref[k]), k
+    assert s["cptr"][-1] == 13 * lat.n
+
+
+def test_exact_trace_bloch_v0(pkg):
+    """kpm_moments_v0 with the full basis (R = N, 20 blocks of 32): sum_r m_n = tr T_n(H~)
+    from the Bloch closed form (periodic V=0 lattice)."""
+    lat, rp, col, val, a, b = problem((4, 4, 5), potential=ZERO_POTENTIAL, periodic_z=True)
+    M = 64
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments_v0(M, np.eye(lat.n, dtype=np.complex128))
+    tr = mu * lat.n
+    x = a * (bloch_energies(lat) - b)
+    ref = np.array([np.cos(n * np.arccos(np.clip(x, -1, 1))).sum() for n in range(M)])
+    assert np.max(np.abs(tr - ref)) / lat.n < 1e-12
+
+
+def test_explicit_v0_matches_oracle(pkg):
+    lat, rp, col, val, a, b = problem((4, 3, 6))
+    rng = np.random.default_rng(0)
+    v0 = rng.normal(size=(lat.n, 3)) + 1j * rng.normal(size=(lat.n, 3))
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments_v0(50, v0)
+    eta_o = oracle.kpm_eta_v0(rp, col, val, a, b, 50, v0)
+    check(eta, mu, eta_o)
+
+
+def test_deterministic(pkg):
+    lat, rp, col, val, a, b = problem((8, 8, 8))
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu1, e1 = ctx.moments(64, 16, 5)
+        mu2, e2 = ctx.moments(64, 16, 5)
+    assert np.array_equal(e1, e2) and np.array_equal(mu1, mu2)
+
+
+def test_errors(pkg):
+    lat, rp, col, val, a, b = problem((3, 3, 2))
+    with pkg.KpmContext() as ctx:
+        with pytest.raises(pkg.KpmError) as ei:
+            ctx.moments(8, 1, 0)
+        assert ei.value.status == pkg.KPM_ESTATE
+        with pytest.raises(pkg.KpmError) as ei:
+            ctx.set_matrix(rp, col, val, -1.0, b)
+        assert ei.value.status == pkg.KPM_EINVAL
+        bad = col.copy()
+        bad[3] = lat.n
+        with pytest.raises(pkg.KpmError) as ei:
+            ctx.set_matrix(rp, bad, val, a, b)
+        assert ei.value.status == pkg.KPM_ERANGE
+        ctx.set_matrix(rp, col, val, a, b)
+        with pytest.raises(pkg.KpmError) as ei:
+            ctx.moments(7, 1, 0)
+        assert ei.value.status == pkg.KPM_EINVAL
+        # a too large: spectrum leaves [-1, 1] -> WDIVERGED warning, results written
+        ctx.set_matrix(rp, col, val, 3 * a, b)
+        mu, _ = ctx.moments(64, 2, 0, allow_warning=True)
+        assert ctx.last_status == pkg.KPM_WDIVERGED
+        z = np.zeros((lat.n, 1), dtype=np.complex128)
+        with pytest.raises(pkg.KpmError) as ei:
+            ctx.moments_v0(8, z, allow=())
+        assert ei.value.status == pkg.KPM_EZERONORM
+
+
+def test_c2_full(pkg):
+    """Config 2 (64x64x32, M=1000, R=8) in the bench launch configuration; the oracle
+    computes the sampled columns 0 and 7 in full."""
+    lat, rp, col, val, a, b = problem((64, 64, 32))
+    M, R = 1000, 8
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments(M, R, SEED)
+    for c in (0, 7):
+        eta_o = oracle.kpm_eta(rp, col, val, a, b, M, 1, SEED, col_begin=c)
+        check(eta[c : c + 1], None, eta_o, cols=[0])
+    assert mu[0] == lat.n and np.all(np.abs(mu) <= mu[0])
+
+
+def test_c3_sampled_columns(pkg):
+    """Config 3 (200x100x40, R=32) at M=200: sampled columns 0 and 31 against the oracle;
+    mu_0 = N and |mu_n| <= mu_0 at full size."""
+    lat, rp, col, val, a, b = problem((200, 100, 40))
+    M, R = 200, 32
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments(M, R, SEED)
+    for c in (0, 31):
+        eta_o = oracle.kpm_eta(rp, col, val, a, b, M, 1, SEED, col_begin=c)
+        check(eta[c : c + 1], None, eta_o, cols=[0])
+    assert mu[0] == lat.n and np.all(np.abs(mu) <= mu[0])
