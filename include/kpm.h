@@ -111,6 +111,12 @@ kpm_status kpm_moments_v0(kpm_ctx* ctx, int M, int R, const double* v0, double* 
  * of one main aug_spmmv sweep (the hot kernel); n_sweeps = main sweeps timed. */
 kpm_status kpm_last_timing(const kpm_ctx* ctx, double* total_ms, double* sweep_ms, int* n_sweeps);
 
+/* Name of the aug_spmmv kernel variant the last kpm_moments* call ran (feed, lanes per row,
+ * unroll), e.g. "staged.lpr16.u4".  "" before the first call.  The
+ * environment variable KPM_VARIANT=<i> (read by kpm_create) selects variant i of a block
+ * width for tuning; the default is variant 0. */
+const char* kpm_last_kernel(const kpm_ctx* ctx);
+
 /* Sizes of the SELL copy, for kpm_export_sell.  n_chunks*C = n_pad. */
 typedef struct {
   int64_t n_loc;     /* local rows                                       */

@@ -20,8 +20,8 @@ STATUS_NAMES = ["KPM_OK", "KPM_EINVAL", "KPM_ESTATE", "KPM_ERANGE", "KPM_ENOMEM"
                 "KPM_EZERONORM", "KPM_WDIVERGED"]
 
 # exported symbols declared in include/kpm.h
-ABI_SYMBOLS = ["kpm_create", "kpm_set_matrix", "kpm_moments", "kpm_moments_v0", "kpm_last_timing",
-               "kpm_get_sell_info", "kpm_export_sell", "kpm_last_error", "kpm_destroy"]
+ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_export_sell", "kpm_get_sell_info", "kpm_last_error",
+               "kpm_last_kernel", "kpm_last_timing", "kpm_moments", "kpm_moments_v0", "kpm_set_matrix"]
 
 
 class KpmError(RuntimeError):
@@ -69,10 +69,12 @@ def load_library():
     lib.kpm_export_sell.argtypes = [P, P, P, P, P, P]
     lib.kpm_last_error.argtypes = [P]
     lib.kpm_last_error.restype = ctypes.c_char_p
+    lib.kpm_last_kernel.argtypes = [P]
+    lib.kpm_last_kernel.restype = ctypes.c_char_p
     lib.kpm_destroy.argtypes = [P]
     lib.kpm_destroy.restype = None
     for name in ABI_SYMBOLS:
-        if name not in ("kpm_last_error", "kpm_destroy"):
+        if name not in ("kpm_last_error", "kpm_last_kernel", "kpm_destroy"):
             getattr(lib, name).restype = i32
     _lib = lib
     return lib
@@ -147,6 +149,9 @@ class KpmContext:
         t, s, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
         self._check(self.lib.kpm_last_timing(self.h, ctypes.byref(t), ctypes.byref(s), ctypes.byref(n)))
         return t.value, s.value, n.value
+
+    def last_kernel(self):
+        return self.lib.kpm_last_kernel(self.h).decode()
 
     def sell_info(self):
         info = kpm_sell_info()

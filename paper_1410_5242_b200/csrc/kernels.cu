@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "kpm_internal.h"
 
 namespace kpm {
@@ -113,133 +115,256 @@ __device__ __forceinline__ void cmac(double2& u, const double2 h, const double2 
   u.y = fma(h.y, x.x, u.y);
 }
 
-template <int R>
-struct Map {
-  static constexpr int LPR = R < 8 ? R : 8;  // lanes per row: LPR*16 B contiguous per row segment
-  static constexpr int CPL = R / LPR;        // block columns per lane
-  static constexpr int RW = 32 / LPR;        // rows per warp (= per row group)
-  static constexpr int U = (CPL >= 4) ? 2 : (CPL == 2 ? 4 : 4);  // j-unroll (loads in flight)
-};
 
 // ------------------------------------------------------------------ aug_spmmv ------
-// Thread mapping: a warp owns a row group of RW consecutive SELL
-// positions inside one chunk; lane = (q, t): q = row in the group, t = lane in the row.
-// Lane t of row q handles block columns r = cc*LPR + t, cc < CPL, so every gathered
-// V row segment is LPR*16 contiguous bytes (a full 128-B line for R >= 8) and each
-// SELL sub-column load of val/col serves RW rows.
-template <int R, bool INIT>
-__global__ void __launch_bounds__(kThreads) aug_spmmv_kernel(const SweepArgs a) {
-  using Mp = Map<R>;
-  constexpr int LPR = Mp::LPR, CPL = Mp::CPL, RW = Mp::RW, U = Mp::U;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int q = lane / LPR;
-  const int t = lane - q * LPR;
-  const uint64_t pol = policy_evict_first();
+// Thread mapping: a warp owns a row group of RW = 32/LPR
+// consecutive SELL positions inside one chunk; lane = (q, t): q = row in the group,
+// t = lane in the row.  Lane t of row q handles block columns r = cc*LPR + t, cc < CPL,
+// so every gathered V row segment is LPR*16 contiguous bytes (a full 128-B line for
+// LPR >= 8) and each SELL sub-column read of val/col serves RW rows.
+//
+// Two matrix feeds:
+//   direct  -- val/col loaded from global (L1 bypass, L2 evict-first); used for R <= 4.
+//   staged  -- one chunk (32 rows) per CTA tile; an elected thread streams the chunk's
+//              val/col block into a 4-stage shared-memory ring with cp.async.bulk (TMA
+//              bulk copy, mbarrier complete_tx), so the only latency left on the
+//              critical path is the V gather.  Used when every chunk fits a stage
+//              (width <= kLcap); otherwise the host selects the direct feed.
 
+constexpr int kStages = 4;
+constexpr int kLcap = 16;                                  // max chunk width staged
+constexpr int kStageValBytes = kC * kLcap * 16;            // 8 KB
+constexpr int kStageColBytes = kC * kLcap * 4;             // 2 KB
+constexpr int kStageBytes = kStageValBytes + kStageColBytes;
+constexpr int kStagedSmem = kStages * kStageBytes;         // 40 KB dynamic
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+template <int R, int LPR, int U>
+struct Cfg {
+  static_assert(R % LPR == 0 && 32 % LPR == 0, "bad lane mapping");
+  static constexpr int CPL = R / LPR;  // block columns per lane
+  static constexpr int RW = 32 / LPR;  // rows per warp (row group)
+};
+
+// Accumulators of the fused dot products of one lane: sum |V|^2, sum conj(W) V.
+template <int CPL>
+struct Dots {
   double ee[CPL], eor[CPL], eoi[CPL];
+  __device__ __forceinline__ void zero() {
 #pragma unroll
-  for (int cc = 0; cc < CPL; ++cc) ee[cc] = eor[cc] = eoi[cc] = 0.0;
+    for (int cc = 0; cc < CPL; ++cc) ee[cc] = eor[cc] = eoi[cc] = 0.0;
+  }
+};
 
-  const int64_t n_groups = a.group_end - a.group_begin;
-  const int64_t seg_groups = (int64_t)a.segment * (kThreads / 32);
-  const int64_t n_segs = (n_groups + seg_groups - 1) / seg_groups;
-  for (int64_t sg = blockIdx.x; sg < n_segs; sg += gridDim.x) {
-    const int64_t g_end = min(n_groups, (sg + 1) * seg_groups);
-    for (int64_t gl = sg * seg_groups + warp; gl < g_end; gl += kThreads / 32) {
-      const int64_t g = a.group_begin + gl;
-      const int64_t p = g * RW + q;       // SELL position of this lane's row
-      const int64_t c = (g * RW) >> 5;    // chunk
-      const int k = (int)(p & 31);
-      const int64_t s0 = __ldg(a.cptr + c);
-      const int len = (int)((__ldg(a.cptr + c + 1) - s0) >> 5);
-      const double2* vp = a.val + s0 + k;
-      const int* cp = a.col + s0 + k;
-      const double2* Vt = a.V + t;
-
-      double2 u[CPL];
+// One row group: u = sum_j H_pj V_j over the chunk's L entries (stored order), then
+// the shift/scale/-W epilogue and the fused dot products (Fig. 5 "&" chain).
+// vp/cp point at entry 0 of this lane's row (stride 32 between entries).
+template <int R, int LPR, int U, bool INIT, bool SMEM>
+__device__ __forceinline__ void row_group(const SweepArgs& a, const double2* vp, const int* cp, int L, int64_t p,
+                                          int t, uint64_t pol, Dots<R / LPR>& d) {
+  using Cf = Cfg<R, LPR, U>;
+  constexpr int CPL = Cf::CPL;
+  const bool live = p < a.n_loc;
+  double2 wo[CPL];
+  if (!INIT && live) {  // old W is streamed from HBM: issue it first so it lands under the gathers
 #pragma unroll
-      for (int cc = 0; cc < CPL; ++cc) u[cc] = make_double2(0.0, 0.0);
-
-      int j = 0;
-      for (; j + U <= len; j += U) {
-        double2 h[U];
-        int cj[U];
+    for (int cc = 0; cc < CPL; ++cc) wo[cc] = ld_stream(a.W + p * R + cc * LPR + t, pol);
+  }
+  double2 u[CPL];
 #pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
+  for (int cc = 0; cc < CPL; ++cc) u[cc] = make_double2(0.0, 0.0);
+  const double2* Vt = a.V + t;
+  for (int j = 0; j < L; j += U) {
+    const int nb = min(U, L - j);
+    double2 h[U];
+    int cj[U];
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+      if (uu < nb) {
+        if (SMEM) {
+          h[uu] = vp[(j + uu) * kC];
+          cj[uu] = cp[(j + uu) * kC];
+        } else {
           h[uu] = ld_stream_nc(vp + (j + uu) * kC, pol);
           cj[uu] = ld_stream_nc(cp + (j + uu) * kC, pol);
         }
-        double2 x[U][CPL];
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu)
-#pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) x[uu][cc] = __ldg(Vt + (int64_t)cj[uu] * R + cc * LPR);
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu)
-#pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h[uu], x[uu][cc]);
-      }
-      for (; j < len; ++j) {
-        const double2 h = ld_stream_nc(vp + j * kC, pol);
-        const int cj = ld_stream_nc(cp + j * kC, pol);
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h, __ldg(Vt + (int64_t)cj * R + cc * LPR));
-      }
-
-      // epilogue: shift, scale, -W, store, fused dot products (Fig. 5 "&" chain)
-      if (p < a.n_loc) {
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-          const int64_t e = p * R + cc * LPR + t;
-          const double2 vi = __ldg(a.V + e);
-          double2 uu = u[cc];
-          uu.x = fma(-a.b, vi.x, uu.x);
-          uu.y = fma(-a.b, vi.y, uu.y);
-          double2 w;
-          if (INIT) {
-            w = make_double2(a.scale * uu.x, a.scale * uu.y);
-          } else {
-            const double2 wo = ld_stream(a.W + e, pol);
-            w = make_double2(fma(a.scale, uu.x, -wo.x), fma(a.scale, uu.y, -wo.y));
-          }
-          st_stream(a.W + e, w, pol);
-          ee[cc] = fma(vi.x, vi.x, fma(vi.y, vi.y, ee[cc]));
-          // conj(w) * v = (wr vr + wi vi) + i (wr vi - wi vr)
-          eor[cc] = fma(w.x, vi.x, fma(w.y, vi.y, eor[cc]));
-          eoi[cc] = fma(w.x, vi.y, fma(-w.y, vi.x, eoi[cc]));
-        }
       }
     }
+    double2 x[U][CPL];
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu)
+      if (uu < nb)
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) x[uu][cc] = __ldg(Vt + (int64_t)cj[uu] * R + cc * LPR);
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu)
+      if (uu < nb)
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h[uu], x[uu][cc]);
   }
+  if (live) {
+#pragma unroll
+    for (int cc = 0; cc < CPL; ++cc) {
+      const int64_t e = p * R + cc * LPR + t;
+      const double2 vi = __ldg(a.V + e);
+      double2 uu = u[cc];
+      uu.x = fma(-a.b, vi.x, uu.x);
+      uu.y = fma(-a.b, vi.y, uu.y);
+      double2 w;
+      if (INIT)
+        w = make_double2(a.scale * uu.x, a.scale * uu.y);
+      else
+        w = make_double2(fma(a.scale, uu.x, -wo[cc].x), fma(a.scale, uu.y, -wo[cc].y));
+      st_stream(a.W + e, w, pol);
+      d.ee[cc] = fma(vi.x, vi.x, fma(vi.y, vi.y, d.ee[cc]));
+      // conj(w) * v = (wr vr + wi vi) + i (wr vi - wi vr)
+      d.eor[cc] = fma(w.x, vi.x, fma(w.y, vi.y, d.eor[cc]));
+      d.eoi[cc] = fma(w.x, vi.y, fma(-w.y, vi.x, d.eoi[cc]));
+    }
+  }
+}
 
-  // ---- CTA reduction (fixed order => deterministic) --------------------------------
+// Warp shuffles over the rows of a warp, then a fixed-order CTA sum -> partials.
+template <int R, int LPR>
+__device__ __forceinline__ void cta_reduce(const SweepArgs& a, Dots<R / LPR>& d, double* red /* [8][3R] */) {
+  constexpr int CPL = R / LPR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int off = LPR; off < 32; off <<= 1) {
 #pragma unroll
     for (int cc = 0; cc < CPL; ++cc) {
-      ee[cc] += __shfl_xor_sync(0xffffffffu, ee[cc], off);
-      eor[cc] += __shfl_xor_sync(0xffffffffu, eor[cc], off);
-      eoi[cc] += __shfl_xor_sync(0xffffffffu, eoi[cc], off);
+      d.ee[cc] += __shfl_xor_sync(0xffffffffu, d.ee[cc], off);
+      d.eor[cc] += __shfl_xor_sync(0xffffffffu, d.eor[cc], off);
+      d.eoi[cc] += __shfl_xor_sync(0xffffffffu, d.eoi[cc], off);
     }
   }
-  __shared__ double red[kThreads / 32][3 * R];
   if (lane < LPR) {
 #pragma unroll
     for (int cc = 0; cc < CPL; ++cc) {
       const int r = cc * LPR + lane;
-      red[warp][r] = ee[cc];
-      red[warp][R + r] = eor[cc];
-      red[warp][2 * R + r] = eoi[cc];
+      red[warp * 3 * R + r] = d.ee[cc];
+      red[warp * 3 * R + R + r] = d.eor[cc];
+      red[warp * 3 * R + 2 * R + r] = d.eoi[cc];
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 3 * R; i += kThreads) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) s += red[w][i];
+    for (int w = 0; w < kThreads / 32; ++w) s += red[w * 3 * R + i];
     a.partials[(int64_t)i * gridDim.x + blockIdx.x] = s;
   }
+}
+
+// Direct feed: grid-stride over row groups.
+template <int R, int LPR, int U, bool INIT>
+__global__ void __launch_bounds__(kThreads) aug_spmmv_direct(const SweepArgs a) {
+  using Cf = Cfg<R, LPR, U>;
+  constexpr int RW = Cf::RW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane / LPR, t = lane - q * LPR;
+  const uint64_t pol = policy_evict_first();
+  Dots<Cf::CPL> d;
+  d.zero();
+  const int64_t g0 = a.chunk_begin * (kC / RW), g1 = a.chunk_end * (kC / RW);
+  for (int64_t g = g0 + blockIdx.x * (int64_t)(kThreads / 32) + warp; g < g1; g += (int64_t)gridDim.x * (kThreads / 32)) {
+    const int64_t p = g * RW + q;
+    const int64_t c = (g * RW) >> 5;
+    const int k = (int)(p & 31);
+    const int64_t s0 = __ldg(a.cptr + c);
+    const int L = (int)((__ldg(a.cptr + c + 1) - s0) >> 5);
+    row_group<R, LPR, U, INIT, false>(a, a.val + s0 + k, a.col + s0 + k, L, p, t, pol, d);
+  }
+  __shared__ double red[(kThreads / 32) * 3 * R];
+  cta_reduce<R, LPR>(a, d, red);
+}
+
+// Staged feed: grid-stride over chunks, TMA bulk copies into a kStages-deep ring.
+template <int R, int LPR, int U, bool INIT>
+__global__ void __launch_bounds__(kThreads, 2) aug_spmmv_staged(const SweepArgs a) {
+  using Cf = Cfg<R, LPR, U>;
+  constexpr int RW = Cf::RW, G = kC / RW;  // row groups per chunk
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ double red[(kThreads / 32) * 3 * R];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane / LPR, t = lane - q * LPR;
+  const uint64_t pol = policy_evict_first();
+  const int64_t n_chunks = a.chunk_end - a.chunk_begin;
+  const int64_t my_tiles = n_chunks > blockIdx.x ? (n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  auto issue = [&](int64_t k) {  // producer: stage tile k (one elected thread)
+    const int s = (int)(k % kStages);
+    const int64_t c = a.chunk_begin + blockIdx.x + k * gridDim.x;
+    const int64_t s0 = a.cptr[c];
+    const int L = (int)((a.cptr[c + 1] - s0) >> 5);
+    const uint32_t bar = smem_u32(&full[s]);
+    const uint32_t vb = (uint32_t)(kC * L * 16), cb = (uint32_t)(kC * L * 4);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect_tx(bar, vb + cb);
+    if (vb) {
+      bulk_g2s(smem_u32(ring + s * kStageBytes), a.val + s0, vb, bar, pol);
+      bulk_g2s(smem_u32(ring + s * kStageBytes + kStageValBytes), a.col + s0, cb, bar, pol);
+    }
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(smem_u32(&full[s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int64_t k = 0; k < kStages && k < my_tiles; ++k) issue(k);
+
+  Dots<Cf::CPL> d;
+  d.zero();
+  for (int64_t k = 0; k < my_tiles; ++k) {
+    const int s = (int)(k % kStages);
+    const int64_t c = a.chunk_begin + blockIdx.x + k * gridDim.x;
+    const int L = (int)((__ldg(a.cptr + c + 1) - __ldg(a.cptr + c)) >> 5);
+    mbar_wait(smem_u32(&full[s]), (uint32_t)((k / kStages) & 1));
+    const double2* sv = reinterpret_cast<const double2*>(ring + s * kStageBytes);
+    const int* sc = reinterpret_cast<const int*>(ring + s * kStageBytes + kStageValBytes);
+    for (int gq = warp; gq < G; gq += kThreads / 32) {
+      const int kr = gq * RW + q;
+      row_group<R, LPR, U, INIT, true>(a, sv + kr, sc + kr, L, c * kC + kr, t, pol, d);
+    }
+    __syncthreads();  // stage s consumed by every warp
+    if (tid == 0 && k + kStages < my_tiles) issue(k + kStages);
+  }
+  cta_reduce<R, LPR>(a, d, red);
 }
 
 // One warp per (sweep, component, column): sum the grid partials in a fixed order.
@@ -268,61 +393,317 @@ __global__ void eta_finalize_kernel(const double* __restrict__ partials, int n_s
   }
 }
 
-template <int R>
-cudaError_t launch_r(bool init, const SweepArgs& a, int grid, cudaStream_t s) {
-  if (init)
-    aug_spmmv_kernel<R, true><<<grid, kThreads, 0, s>>>(a);
-  else
-    aug_spmmv_kernel<R, false><<<grid, kThreads, 0, s>>>(a);
-  return cudaGetLastError();
+// ------------------------------------------------------------- tiled feed --------
+// One chunk (32 rows) per CTA tile.  Warp 0 streams the whole working set of the tile into
+// a shared-memory ring with cp.async.bulk (TMA bulk copies, one mbarrier per stage):
+//   [V rows of the tile: own 32 rows | the chunk's other distinct columns, as runs]
+//   [W of the 32 own rows (main sweep)] [val block] [lcol block (uint16 tile-row index)]
+// so every gathered V row is fetched from L2/HBM once per chunk and no gather occupies a
+// register while in flight.  All warps then compute from shared memory.
+constexpr int kMaxTileStages = 4;
+constexpr int kTileBudget = 232448 - 8192;  // minus static smem (reduction buffer, barriers)  // 227 KB dynamic shared memory minus margin
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, v, off);
+    if (lane >= off) v += n;
+  }
+  return v;
 }
 
-template <int R>
-int occupancy_r(bool init) {
-  int n = 0;
-  if (init)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_kernel<R, true>, kThreads, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_kernel<R, false>, kThreads, 0);
-  return n;
+constexpr int kTiledThreads = kThreads + 32;  // 8 consumer warps + 1 producer warp
+
+template <int R, int LPR, int U, bool INIT>
+__global__ void __launch_bounds__(kTiledThreads, 1) aug_spmmv_tiled(const SweepArgs a) {
+  using Cf = Cfg<R, LPR, U>;
+  constexpr int RW = Cf::RW, G = kC / RW, CPL = Cf::CPL;
+  constexpr int NCW = kThreads / 32;  // consumer warps
+  constexpr int ROWB = R * 16;        // bytes per V/W row
+  extern __shared__ __align__(128) unsigned char tsm[];
+  __shared__ __align__(8) uint64_t full[kMaxTileStages], empty[kMaxTileStages];
+  __shared__ int tile_len[kMaxTileStages];
+  __shared__ double red[NCW * 3 * R];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const TileLayout tl = a.tl;
+  const int64_t n_chunks = a.chunk_end - a.chunk_begin;
+  const int64_t my_tiles = n_chunks > blockIdx.x ? (n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const uint64_t pol = policy_evict_first();
+
+  if (tid == 0) {
+    for (int s = 0; s < tl.stages; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  Dots<CPL> d;
+  d.zero();
+  if (warp == NCW) {
+    // ---------------- producer warp: TMA bulk copies of tile k into stage k % S ----------
+    // Lane i < 16 holds slot i of the chunk's copy record (header + up to 15 bulk copies);
+    // the record of tile k+1 is loaded while tile k is issued, so no metadata load sits on
+    // the producer's critical path.
+    auto load_rec = [&](int64_t k) -> uint4 {
+      const int64_t c = a.chunk_begin + blockIdx.x + k * gridDim.x;
+      return lane < 16 ? __ldg(a.rec + c * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    uint4 nxt = my_tiles > 0 ? load_rec(0) : make_uint4(0u, 0u, 0u, 0u);
+    for (int64_t k = 0; k < my_tiles; ++k) {
+      const uint4 cur = nxt;
+      if (k + 1 < my_tiles) nxt = load_rec(k + 1);
+      const int s = (int)(k % tl.stages);
+      const uint32_t total = __shfl_sync(0xffffffffu, INIT ? cur.y : cur.x, 0);
+      const uint32_t L = __shfl_sync(0xffffffffu, cur.z, 0);
+      const uint32_t ncmd = __shfl_sync(0xffffffffu, cur.w, 0);
+      if (k >= tl.stages) mbar_wait(smem_u32(&empty[s]), (uint32_t)(((k / tl.stages) - 1) & 1));
+      unsigned char* st = tsm + (size_t)s * tl.stage_bytes;
+      const uint32_t bar = smem_u32(&full[s]);
+      if (lane == 0) {
+        tile_len[s] = (int)L;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(bar, total);
+      }
+      __syncwarp();
+      if (lane >= 1 && (uint32_t)lane <= ncmd) {
+        const uint32_t base = cur.w >> 28, bytes = cur.w & 0x0FFFFFFFu;
+        const int64_t off = (int64_t)(((uint64_t)cur.y << 32) | cur.x);
+        if (!(INIT && base == 1)) {
+          const unsigned char* src = base == 0   ? reinterpret_cast<const unsigned char*>(a.V)
+                                     : base == 1 ? reinterpret_cast<const unsigned char*>(a.W)
+                                     : base == 2 ? reinterpret_cast<const unsigned char*>(a.val)
+                                                 : reinterpret_cast<const unsigned char*>(a.lcol);
+          bulk_g2s(smem_u32(st + cur.z), src + off, bytes, bar, base == 0 ? 0ull : pol);
+        }
+      }
+    }
+  } else {
+    // ---------------- consumer warps ---------------------------------------------------
+    const int q = lane / LPR, t = lane - q * LPR;
+    for (int64_t k = 0; k < my_tiles; ++k) {
+      const int s = (int)(k % tl.stages);
+      const int64_t c = a.chunk_begin + blockIdx.x + k * gridDim.x;
+      const unsigned char* st = tsm + (size_t)s * tl.stage_bytes;
+      const double2* sV = reinterpret_cast<const double2*>(st);
+      const double2* sW = reinterpret_cast<const double2*>(st + tl.off_w);
+      const double2* sval = reinterpret_cast<const double2*>(st + tl.off_val);
+      const uint16_t* slc = reinterpret_cast<const uint16_t*>(st + tl.off_lcol);
+      mbar_wait(smem_u32(&full[s]), (uint32_t)((k / tl.stages) & 1));
+      const int L = tile_len[s];
+      for (int gq = warp; gq < G; gq += NCW) {
+        const int kr = gq * RW + q;
+        const int64_t p = c * kC + kr;
+        double2 u[CPL];
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) u[cc] = make_double2(0.0, 0.0);
+        for (int j = 0; j < L; j += U) {
+          const int nb = min(U, L - j);
+          double2 h[U];
+          int li[U];
+#pragma unroll
+          for (int uu = 0; uu < U; ++uu)
+            if (uu < nb) {
+              h[uu] = sval[(j + uu) * kC + kr];
+              li[uu] = slc[(j + uu) * kC + kr];
+            }
+#pragma unroll
+          for (int uu = 0; uu < U; ++uu)
+            if (uu < nb)
+#pragma unroll
+              for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h[uu], sV[li[uu] * R + cc * LPR + t]);
+        }
+        if (p < a.n_loc) {
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) {
+            const int col = cc * LPR + t;
+            const double2 vi = sV[kr * R + col];
+            double2 uu = u[cc];
+            uu.x = fma(-a.b, vi.x, uu.x);
+            uu.y = fma(-a.b, vi.y, uu.y);
+            double2 w;
+            if (INIT) {
+              w = make_double2(a.scale * uu.x, a.scale * uu.y);
+            } else {
+              const double2 wo = sW[kr * R + col];
+              w = make_double2(fma(a.scale, uu.x, -wo.x), fma(a.scale, uu.y, -wo.y));
+            }
+            st_stream(a.W + p * R + col, w, pol);
+            d.ee[cc] = fma(vi.x, vi.x, fma(vi.y, vi.y, d.ee[cc]));
+            d.eor[cc] = fma(w.x, vi.x, fma(w.y, vi.y, d.eor[cc]));
+            d.eoi[cc] = fma(w.x, vi.y, fma(-w.y, vi.x, d.eoi[cc]));
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&empty[s]));  // stage s released by this warp
+    }
+    // warp-level part of the dot-product reduction
+#pragma unroll
+    for (int off = LPR; off < 32; off <<= 1) {
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) {
+        d.ee[cc] += __shfl_xor_sync(0xffffffffu, d.ee[cc], off);
+        d.eor[cc] += __shfl_xor_sync(0xffffffffu, d.eor[cc], off);
+        d.eoi[cc] += __shfl_xor_sync(0xffffffffu, d.eoi[cc], off);
+      }
+    }
+    if (lane < LPR) {
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) {
+        const int r = cc * LPR + lane;
+        red[warp * 3 * R + r] = d.ee[cc];
+        red[warp * 3 * R + R + r] = d.eor[cc];
+        red[warp * 3 * R + 2 * R + r] = d.eoi[cc];
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < 3 * R; i += kTiledThreads) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < NCW; ++w) sum += red[w * 3 * R + i];
+    a.partials[(int64_t)i * gridDim.x + blockIdx.x] = sum;
+  }
+}
+
+enum Feed { kDirect = 0, kStaged = 1, kTiled = 2 };
+
+template <int R, int LPR, int U, int FEED>
+struct Variant {
+  static cudaError_t launch(bool init, const SweepArgs& a, int grid, cudaStream_t s) {
+    if constexpr (FEED == kStaged) {
+      if (init)
+        aug_spmmv_staged<R, LPR, U, true><<<grid, kThreads, kStagedSmem, s>>>(a);
+      else
+        aug_spmmv_staged<R, LPR, U, false><<<grid, kThreads, kStagedSmem, s>>>(a);
+    } else if constexpr (FEED == kTiled) {
+      const int smem = a.tl.stages * a.tl.stage_bytes;
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (init)
+        aug_spmmv_tiled<R, LPR, U, true><<<grid, kTiledThreads, smem, s>>>(a);
+      else
+        aug_spmmv_tiled<R, LPR, U, false><<<grid, kTiledThreads, smem, s>>>(a);
+    } else {
+      if (init)
+        aug_spmmv_direct<R, LPR, U, true><<<grid, kThreads, 0, s>>>(a);
+      else
+        aug_spmmv_direct<R, LPR, U, false><<<grid, kThreads, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+  }
+  static int occupancy(int dyn_smem) {
+    int n = 0;
+    if constexpr (FEED == kStaged) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_staged<R, LPR, U, false>, kThreads, kStagedSmem);
+    } else if constexpr (FEED == kTiled) {
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_tiled<R, LPR, U, false>, kTiledThreads, dyn_smem);
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_direct<R, LPR, U, false>, kThreads, 0);
+    }
+    return n;
+  }
+};
+
+typedef cudaError_t (*LaunchFn)(bool, const SweepArgs&, int, cudaStream_t);
+typedef int (*OccFn)(int);
+struct Entry {
+  int R;
+  const char* name;
+  int feed;
+  LaunchFn launch;
+  OccFn occ;
+};
+#define KPM_VARIANT(R, LPR, U, F, NAME) {R, NAME, F, Variant<R, LPR, U, F>::launch, Variant<R, LPR, U, F>::occupancy}
+// First entry of each width is the default (chosen from the B200 measurements in DESIGN.md).
+const Entry kTable[] = {
+    KPM_VARIANT(1, 1, 4, kDirect, "direct.lpr1.u4"),
+    KPM_VARIANT(1, 1, 8, kDirect, "direct.lpr1.u8"),
+    KPM_VARIANT(2, 2, 4, kDirect, "direct.lpr2.u4"),
+    KPM_VARIANT(2, 2, 8, kDirect, "direct.lpr2.u8"),
+    KPM_VARIANT(4, 4, 4, kDirect, "direct.lpr4.u4"),
+    KPM_VARIANT(4, 4, 8, kDirect, "direct.lpr4.u8"),
+    KPM_VARIANT(8, 8, 4, kTiled, "tiled.lpr8.u4"),
+    KPM_VARIANT(8, 8, 4, kStaged, "staged.lpr8.u4"),
+    KPM_VARIANT(8, 8, 8, kTiled, "tiled.lpr8.u8"),
+    KPM_VARIANT(8, 8, 4, kDirect, "direct.lpr8.u4"),
+    KPM_VARIANT(16, 8, 4, kTiled, "tiled.lpr8.u4"),
+    KPM_VARIANT(16, 16, 4, kTiled, "tiled.lpr16.u4"),
+    KPM_VARIANT(16, 8, 4, kStaged, "staged.lpr8.u4"),
+    KPM_VARIANT(16, 8, 4, kDirect, "direct.lpr8.u4"),
+    KPM_VARIANT(32, 8, 4, kTiled, "tiled.lpr8.u4"),
+    KPM_VARIANT(32, 16, 4, kTiled, "tiled.lpr16.u4"),
+    KPM_VARIANT(32, 32, 4, kTiled, "tiled.lpr32.u4"),
+    KPM_VARIANT(32, 8, 2, kTiled, "tiled.lpr8.u2"),
+    KPM_VARIANT(32, 16, 4, kStaged, "staged.lpr16.u4"),
+    KPM_VARIANT(32, 8, 2, kDirect, "direct.lpr8.u2"),
+};
+
+const Entry* find(int R, int variant) {
+  int i = 0;
+  for (const Entry& e : kTable)
+    if (e.R == R && i++ == variant) return &e;
+  return nullptr;
 }
 
 }  // namespace
 
-int rows_per_group(int R) {
-  switch (R) {
-    case 1: return Map<1>::RW;
-    case 2: return Map<2>::RW;
-    case 4: return Map<4>::RW;
-    case 8: return Map<8>::RW;
-    case 16: return Map<16>::RW;
-    case 32: return Map<32>::RW;
-  }
-  return 0;
+int variant_count(int R) {
+  int n = 0;
+  for (const Entry& e : kTable) n += (e.R == R);
+  return n;
 }
 
-int sweep_occupancy(int R, bool init) {
-  switch (R) {
-    case 1: return occupancy_r<1>(init);
-    case 2: return occupancy_r<2>(init);
-    case 4: return occupancy_r<4>(init);
-    case 8: return occupancy_r<8>(init);
-    case 16: return occupancy_r<16>(init);
-    case 32: return occupancy_r<32>(init);
-  }
-  return 0;
+const char* variant_name(int R, int variant) {
+  const Entry* e = find(R, variant);
+  return e ? e->name : nullptr;
 }
 
-cudaError_t launch_aug_spmmv(int R, bool init, const SweepArgs& a, int grid, cudaStream_t s) {
-  switch (R) {
-    case 1: return launch_r<1>(init, a, grid, s);
-    case 2: return launch_r<2>(init, a, grid, s);
-    case 4: return launch_r<4>(init, a, grid, s);
-    case 8: return launch_r<8>(init, a, grid, s);
-    case 16: return launch_r<16>(init, a, grid, s);
-    case 32: return launch_r<32>(init, a, grid, s);
-  }
-  return cudaErrorInvalidValue;
+bool variant_staged(int R, int variant) {
+  const Entry* e = find(R, variant);
+  return e && e->feed == kStaged;
+}
+
+bool variant_tiled(int R, int variant) {
+  const Entry* e = find(R, variant);
+  return e && e->feed == kTiled;
+}
+
+static int round128(int64_t b) { return (int)((b + 127) / 128 * 128); }
+
+TileLayout plan_tiles(int R, int64_t max_other, int64_t max_width, int stages) {
+  TileLayout tl;
+  const int64_t v = round128((kC + max_other) * R * 16);
+  const int64_t w = round128(kC * R * 16);
+  const int64_t val = round128(kC * max_width * 16);
+  const int64_t lc = round128(kC * max_width * 2);
+  const int64_t stage = v + w + val + lc;
+  // Two stages by default: more CTAs per SM (more producer streams and consumer warps)
+  // beat a deeper ring (B200 measurements).  `stages` may lower it.
+  int n = (int)std::min<int64_t>(stages > 0 ? stages : 2, kTileBudget / std::max<int64_t>(stage, 1));
+  if (n < 1) return tl;
+  tl.stages = n;
+  tl.stage_bytes = (int)stage;
+  tl.off_w = (int)v;
+  tl.off_val = (int)(v + w);
+  tl.off_lcol = (int)(v + w + val);
+  return tl;
+}
+
+int staged_max_width() { return kLcap; }
+
+int sweep_occupancy(int R, int variant, int dyn_smem) {
+  const Entry* e = find(R, variant);
+  return e ? e->occ(dyn_smem) : 0;
+}
+
+cudaError_t launch_aug_spmmv(int R, int variant, bool init, const SweepArgs& a, int grid, cudaStream_t s) {
+  const Entry* e = find(R, variant);
+  if (!e) return cudaErrorInvalidValue;
+  return e->launch(init, a, grid, s);
 }
 
 static int elementwise_grid(int64_t n_el) {

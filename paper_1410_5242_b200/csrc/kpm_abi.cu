@@ -25,8 +25,10 @@ struct kpm_ctx {
   bool sticky = false;
   std::string err;
   int num_sms = 148;
-  int segment = 1;       // chunk-schedule segment (tuning knob, env KPM_SEGMENT)
-  int grid_per_sm = 0;   // 0 -> occupancy (env KPM_GRID_PER_SM)
+  int variant_override = -1;  // tuning knob: env KPM_VARIANT (index into the width's variants)
+  int grid_per_sm = 0;        // 0 -> occupancy (env KPM_GRID_PER_SM)
+  int tile_stages = 0;        // 0 -> as many as fit (env KPM_TILE_STAGES)
+  std::string last_variant;
 
   // matrix
   bool have_matrix = false;
@@ -34,6 +36,8 @@ struct kpm_ctx {
   double a = 0.0, b = 0.0;
   DevSell sell;
   std::vector<int64_t> halo;  // global ids of halo slots
+  HostTiles tiles;            // runs of the tiled feed (host copy, for the per-R records)
+  std::vector<int64_t> cptr_h;
 
   // work buffers (grow-only)
   double2* X0 = nullptr;
@@ -110,20 +114,20 @@ extern "C" kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt) {
     kpm_destroy(ctx);
     return KPM_ECUDA;
   }
-  ctx->segment = std::max(1, env_int("KPM_SEGMENT", 1));
+  ctx->variant_override = env_int("KPM_VARIANT", -1);
   ctx->grid_per_sm = std::max(0, env_int("KPM_GRID_PER_SM", 0));
+  ctx->tile_stages = std::max(0, env_int("KPM_TILE_STAGES", 0));
   *out = ctx;
   return KPM_OK;
 }
+
+static void free_sell(DevSell& s);
 
 extern "C" void kpm_destroy(kpm_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->opt.device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  cudaFree(ctx->sell.val);
-  cudaFree(ctx->sell.col);
-  cudaFree(ctx->sell.cptr);
-  cudaFree(ctx->sell.perm);
+  free_sell(ctx->sell);
   cudaFree(ctx->X0);
   cudaFree(ctx->X1);
   cudaFree(ctx->partials);
@@ -146,6 +150,8 @@ static void free_sell(DevSell& s) {
   cudaFree(s.col);
   cudaFree(s.cptr);
   cudaFree(s.perm);
+  cudaFree(s.lcol);
+  for (int i = 0; i < 6; ++i) cudaFree(s.rec[i]);
   s = DevSell();
 }
 
@@ -206,6 +212,8 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
   d.n_chunks = hs.n_chunks;
   d.n_slots = hs.cptr[hs.n_chunks];
   d.n_halo = hs.n_halo;
+  d.max_width = 0;
+  for (int64_t c = 0; c < hs.n_chunks; ++c) d.max_width = std::max(d.max_width, (hs.cptr[c + 1] - hs.cptr[c]) / hs.C);
   auto alloc = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
   cudaError_t e = alloc((void**)&d.val, sizeof(double2) * d.n_slots);
   if (e == cudaSuccess) e = alloc((void**)&d.col, sizeof(int) * d.n_slots);
@@ -220,6 +228,25 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
   KPM_CUDA(cudaMemcpy(d.col, hs.col.data(), sizeof(int) * d.n_slots, cudaMemcpyHostToDevice));
   KPM_CUDA(cudaMemcpy(d.cptr, hs.cptr.data(), sizeof(int64_t) * (d.n_chunks + 1), cudaMemcpyHostToDevice));
   KPM_CUDA(cudaMemcpy(d.perm, hs.perm.data(), sizeof(int) * d.n_loc, cudaMemcpyHostToDevice));
+  // gather plan of the tiled feed (copy records are built per block width on first use)
+  {
+    build_tiles_host(hs, ctx->tiles);
+    d.tiles_ok = ctx->tiles.ok;
+    d.max_other = ctx->tiles.max_other;
+    d.max_runs = ctx->tiles.max_runs;
+    ctx->cptr_h = hs.cptr;
+    if (d.tiles_ok) {
+      if (alloc((void**)&d.lcol, sizeof(uint16_t) * ctx->tiles.lcol.size()) != cudaSuccess) {
+        cudaGetLastError();
+        d.lcol = nullptr;
+        d.tiles_ok = false;  // the other feeds still work
+      } else {
+        KPM_CUDA(cudaMemcpy(d.lcol, ctx->tiles.lcol.data(), sizeof(uint16_t) * ctx->tiles.lcol.size(),
+                            cudaMemcpyHostToDevice));
+      }
+    }
+    std::vector<uint16_t>().swap(ctx->tiles.lcol);  // host copy no longer needed
+  }
   ctx->halo = hs.halo;
   ctx->n_global = H->n_global;
   ctx->row_begin = H->row_begin;
@@ -265,11 +292,35 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   if ((st = ensure(ctx, (void**)&ctx->X1, &xcap, (size_t)n_rows_total * Rk, sizeof(double2))) != KPM_OK) return st;
   ctx->x_cap = xcap;
 
-  const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, sweep_occupancy(Rk, false));
-  const int rpg = rows_per_group(Rk);
-  const int64_t n_groups = s.n_pad / rpg;
-  const int64_t n_segs = (n_groups + 8LL * ctx->segment - 1) / (8LL * ctx->segment);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * occ, n_segs));
+  TileLayout plan = s.tiles_ok ? plan_tiles(Rk, s.max_other, s.max_width, std::min(ctx->tile_stages, 4)) : TileLayout();
+  const int lg = __builtin_ctz(Rk);
+  if (plan.stages >= 1 && !ctx->sell.rec[lg] && !ctx->sell.rec_failed[lg]) {
+    std::vector<uint32_t> rec;
+    if (!build_tile_records(ctx->cptr_h, ctx->tiles, Rk, plan.off_w, plan.off_val, plan.off_lcol, rec)) {
+      ctx->sell.rec_failed[lg] = true;
+    } else {
+      size_t cap = 0;
+      st = ensure(ctx, (void**)&ctx->sell.rec[lg], &cap, rec.size() / 4, sizeof(uint4));
+      if (st != KPM_OK) return st;
+      KPM_CUDA(cudaMemcpy(ctx->sell.rec[lg], rec.data(), sizeof(uint32_t) * rec.size(), cudaMemcpyHostToDevice));
+    }
+  }
+  if (!ctx->sell.rec[lg]) plan = TileLayout();
+  auto usable = [&](int v) {
+    if (variant_tiled(Rk, v)) return plan.stages >= 1;
+    if (variant_staged(Rk, v)) return s.max_width <= staged_max_width();
+    return true;
+  };
+  int variant = 0;
+  if (ctx->variant_override >= 0 && ctx->variant_override < variant_count(Rk)) variant = ctx->variant_override;
+  if (!usable(variant))
+    for (variant = 0; variant < variant_count(Rk) - 1 && !usable(variant); ++variant) {
+    }
+  ctx->last_variant = variant_name(Rk, variant);
+  const TileLayout tl = plan;
+  const int dyn_smem = variant_tiled(Rk, variant) ? tl.stages * tl.stage_bytes : 0;
+  const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, sweep_occupancy(Rk, variant, dyn_smem));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * occ, s.n_chunks));
   const size_t per_sweep = (size_t)3 * Rk * grid;
   if ((st = ensure(ctx, (void**)&ctx->partials, &ctx->partials_cap, per_sweep * n_sweeps, sizeof(double))) != KPM_OK)
     return st;
@@ -307,16 +358,18 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   sa.col = s.col;
   sa.cptr = s.cptr;
   sa.n_loc = s.n_loc;
-  sa.group_begin = 0;
-  sa.group_end = n_groups;
-  sa.segment = ctx->segment;
+  sa.chunk_begin = 0;
+  sa.chunk_end = s.n_chunks;
+  sa.rec = s.rec[lg];
+  sa.lcol = s.lcol;
+  sa.tl = tl;
   sa.b = ctx->b;
   // a2: init sweep  W = a(H - b)V, eta_0, eta_1
   sa.V = ctx->X0;
   sa.W = ctx->X1;
   sa.scale = ctx->a;
   sa.partials = ctx->partials;
-  KPM_CUDA(launch_aug_spmmv(Rk, true, sa, grid, str));
+  KPM_CUDA(launch_aug_spmmv(Rk, variant, true, sa, grid, str));
   // a3: main sweeps  W <- 2a(H - b)V - W, eta_2m, eta_2m+1
   KPM_CUDA(cudaEventRecord(ctx->ev[1], str));
   sa.scale = 2.0 * ctx->a;
@@ -324,7 +377,7 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     sa.V = (m & 1) ? ctx->X1 : ctx->X0;
     sa.W = (m & 1) ? ctx->X0 : ctx->X1;
     sa.partials = ctx->partials + per_sweep * m;
-    KPM_CUDA(launch_aug_spmmv(Rk, false, sa, grid, str));
+    KPM_CUDA(launch_aug_spmmv(Rk, variant, false, sa, grid, str));
   }
   KPM_CUDA(cudaEventRecord(ctx->ev[2], str));
   // a4: deterministic grid reduction of all sweeps' partials
@@ -424,6 +477,8 @@ extern "C" kpm_status kpm_last_timing(const kpm_ctx* ctx, double* total_ms, doub
   if (n_sweeps) *n_sweeps = ctx->last_n_sweeps;
   return KPM_OK;
 }
+
+extern "C" const char* kpm_last_kernel(const kpm_ctx* ctx) { return ctx ? ctx->last_variant.c_str() : ""; }
 
 extern "C" kpm_status kpm_get_sell_info(const kpm_ctx* ctx, kpm_sell_info* info) {
   if (!ctx || !info) return KPM_EINVAL;

@@ -20,6 +20,20 @@ struct DevSell {
   int64_t* cptr = nullptr; // n_chunks+1
   int* perm = nullptr;     // n_loc: local row stored at position p
   int64_t n_loc = 0, n_pad = 0, n_chunks = 0, n_slots = 0, n_halo = 0;
+  int64_t max_width = 0;   // widest chunk (entries per row)
+  // tiled feed (TMA gather plan, see sell_build.h HostTiles)
+  bool tiles_ok = false;
+  uint16_t* lcol = nullptr;    // n_slots: column as index into the chunk's shared-memory tile
+  int64_t max_other = 0, max_runs = 0;
+  uint4* rec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // copy records per log2(R)
+  bool rec_failed[6] = {false, false, false, false, false, false};
+};
+
+// Shared-memory layout of one stage of the tiled feed (bytes, 128-B aligned sections).
+struct TileLayout {
+  int stages = 0;
+  int stage_bytes = 0;
+  int off_w = 0, off_val = 0, off_lcol = 0;  // V tile rows start at 0
 };
 
 // One aug_spmmv sweep over the row groups [group_begin, group_end).
@@ -30,11 +44,14 @@ struct SweepArgs {
   const double2* V;    // nu_m   (read only)
   double2* W;          // nu_{m-1} in, nu_{m+1} out
   int64_t n_loc;
-  int64_t group_begin, group_end;
-  int segment;         // consecutive 8-group steps a CTA takes before jumping (chunk schedule)
+  int64_t chunk_begin, chunk_end;  // SELL chunks swept by this launch
   double scale;        // 2a for the main sweep, a for the init sweep
   double b;
   double* partials;    // [3R][gridDim]: per-CTA (eta_even, Re eta_odd, Im eta_odd) of this sweep
+  // tiled feed only
+  const uint4* rec;      // kRecSlots per chunk (sell_build.h)
+  const uint16_t* lcol;
+  TileLayout tl;
 };
 
 // Launch helpers (kernels.cu).  All return cudaGetLastError() of the launch.
@@ -44,9 +61,16 @@ cudaError_t launch_z4_init(double2* V, double2* W, const int* perm, int64_t n_lo
 cudaError_t launch_v0_upload_permute(double2* V, double2* W, const double2* v0_dev, const int* perm,
                                      int64_t n_loc, int64_t n_rows_total, int R, int r_valid,
                                      cudaStream_t s);
-cudaError_t launch_aug_spmmv(int R, bool init, const SweepArgs& a, int grid, cudaStream_t s);
-int rows_per_group(int R);
-int sweep_occupancy(int R, bool init);
+// Kernel variants per block width R (feed x lanes-per-row x unroll); variant 0 is the default.
+int variant_count(int R);
+const char* variant_name(int R, int variant);
+int sweep_occupancy(int R, int variant, int dyn_smem);
+bool variant_staged(int R, int variant);
+int staged_max_width();  // widest chunk (entries per row) the staged feed accepts
+bool variant_tiled(int R, int variant);
+// Shared-memory plan of the tiled feed for block width R, or stages == 0 if it does not fit.
+TileLayout plan_tiles(int R, int64_t max_other, int64_t max_width, int stages);  // stages 0 = default
+cudaError_t launch_aug_spmmv(int R, int variant, bool init, const SweepArgs& a, int grid, cudaStream_t s);
 // eta[m][r] (double2) for m in [0, n_sweeps) from partials[m][3R][grid]
 cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int grid, double2* eta_even,
                                 double2* eta_odd, cudaStream_t s);

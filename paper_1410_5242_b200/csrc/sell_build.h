@@ -16,6 +16,28 @@ struct HostSell {
   std::vector<int64_t> halo;   // n_halo global ids, ascending
 };
 
+// Per-chunk gather plan of the TMA-fed ("tiled") sweep kernel: the distinct columns a chunk
+// reads that are not its own 32 rows, as maximal runs of consecutive rows (ascending), and
+// every SELL slot's column re-expressed as an index into the chunk's shared-memory tile
+// [own rows 0..31 | run rows in order].
+struct HostTiles {
+  bool ok = false;                 // false: some chunk needs > 65535 tile rows
+  std::vector<int64_t> run_ptr;    // n_chunks+1, into runs
+  std::vector<int32_t> runs;       // 2 per run: first row, row count
+  std::vector<uint16_t> lcol;      // n_slots
+  int64_t max_other = 0;           // max rows outside the own block, over chunks
+  int64_t max_runs = 0;
+};
+void build_tiles_host(const HostSell& s, HostTiles& out);
+
+// Copy-command records of the tiled feed for block width R: 16 x 16-byte slots per chunk.
+// Slot 0 = {bytes (main sweep), bytes (init sweep, no W), chunk width L, n_cmd}; slots
+// 1..n_cmd = {src byte offset lo, hi, dst byte offset in the stage, bytes | base << 28} with
+// base 0 = V, 1 = W, 2 = val, 3 = lcol.  Returns false if a chunk needs more than 15 copies.
+constexpr int kRecSlots = 16;
+bool build_tile_records(const std::vector<int64_t>& cptr, const HostTiles& t, int R, int off_w, int off_val,
+                        int off_lcol, std::vector<uint32_t>& rec);
+
 // Returns 0 or a kpm_status code (err filled).
 int build_sell_host(const int64_t* row_ptr, const int64_t* col, const double* val, int64_t n_loc,
                     int64_t row_begin, int64_t row_end, int C, int sigma, HostSell& out, std::string& err);
