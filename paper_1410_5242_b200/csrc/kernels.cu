@@ -412,18 +412,29 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
-constexpr int kTiledThreads = kThreads + 32;  // 8 consumer warps + 1 producer warp
+// CS = column split: CS consumer warps share a row group, each owning CPL/CS of the lane's
+// block columns (more warps in flight for the same registers; val/lcol reads repeat CS times).
+// Consumer warps per column part: one per row group of a chunk, at most 8 (so R < 8 uses
+// small CTAs: G = LPR row groups of 32/LPR rows each).
+template <int LPR>
+__host__ __device__ constexpr int tiled_ncwg() { return LPR < 8 ? LPR : 8; }
+template <int LPR, int CS>
+__host__ __device__ constexpr int tiled_threads() { return 32 * (tiled_ncwg<LPR>() * CS + 1); }
 
-template <int R, int LPR, int U, bool INIT>
-__global__ void __launch_bounds__(kTiledThreads, 1) aug_spmmv_tiled(const SweepArgs a) {
+template <int R, int LPR, int U, int CS, bool INIT>
+__global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(const SweepArgs a) {
   using Cf = Cfg<R, LPR, U>;
-  constexpr int RW = Cf::RW, G = kC / RW, CPL = Cf::CPL;
-  constexpr int NCW = kThreads / 32;  // consumer warps
-  constexpr int ROWB = R * 16;        // bytes per V/W row
+  constexpr int RW = Cf::RW, G = kC / RW;
+  static_assert(Cf::CPL % CS == 0, "column split must divide the columns per lane");
+  constexpr int CPL = Cf::CPL / CS;       // block columns per lane in this warp
+  constexpr int NCWG = tiled_ncwg<LPR>(); // consumer warps per column part
+  constexpr int NCW = NCWG * CS;          // consumer warps
+  constexpr int kTiledThreads = tiled_threads<LPR, CS>();
+  constexpr int ROWB = R * 16;            // bytes per V/W row
   extern __shared__ __align__(128) unsigned char tsm[];
   __shared__ __align__(8) uint64_t full[kMaxTileStages], empty[kMaxTileStages];
   __shared__ int tile_len[kMaxTileStages];
-  __shared__ double red[NCW * 3 * R];
+  __shared__ double red[NCWG * 3 * R];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const TileLayout tl = a.tl;
   const int64_t n_chunks = a.chunk_end - a.chunk_begin;
@@ -481,7 +492,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) aug_spmmv_tiled(const SweepA
     }
   } else {
     // ---------------- consumer warps ---------------------------------------------------
-    const int q = lane / LPR, t = lane - q * LPR;
+    const int q = lane / LPR;
+    const int g0 = warp % NCWG, part = warp / NCWG;
+    const int t = lane - q * LPR + part * CPL * LPR;  // first block column of this lane
     for (int64_t k = 0; k < my_tiles; ++k) {
       const int s = (int)(k % tl.stages);
       const int64_t c = a.chunk_begin + blockIdx.x + k * gridDim.x;
@@ -492,27 +505,39 @@ __global__ void __launch_bounds__(kTiledThreads, 1) aug_spmmv_tiled(const SweepA
       const uint16_t* slc = reinterpret_cast<const uint16_t*>(st + tl.off_lcol);
       mbar_wait(smem_u32(&full[s]), (uint32_t)((k / tl.stages) & 1));
       const int L = tile_len[s];
-      for (int gq = warp; gq < G; gq += NCW) {
+      for (int gq = g0; gq < G; gq += NCWG) {
         const int kr = gq * RW + q;
         const int64_t p = c * kC + kr;
         double2 u[CPL];
 #pragma unroll
         for (int cc = 0; cc < CPL; ++cc) u[cc] = make_double2(0.0, 0.0);
-        for (int j = 0; j < L; j += U) {
-          const int nb = min(U, L - j);
+        const double2* sv = sval + kr;
+        const uint16_t* sl = slc + kr;
+        const double2* sVt = sV + t;
+        int j = 0;
+        for (; j + U <= L; j += U) {  // full batches: no predication
           double2 h[U];
           int li[U];
 #pragma unroll
-          for (int uu = 0; uu < U; ++uu)
-            if (uu < nb) {
-              h[uu] = sval[(j + uu) * kC + kr];
-              li[uu] = slc[(j + uu) * kC + kr];
-            }
+          for (int uu = 0; uu < U; ++uu) {
+            h[uu] = sv[(j + uu) * kC];
+            li[uu] = sl[(j + uu) * kC] * R;
+          }
+          double2 x[U][CPL];
 #pragma unroll
           for (int uu = 0; uu < U; ++uu)
-            if (uu < nb)
 #pragma unroll
-              for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h[uu], sV[li[uu] * R + cc * LPR + t]);
+            for (int cc = 0; cc < CPL; ++cc) x[uu][cc] = sVt[li[uu] + cc * LPR];
+#pragma unroll
+          for (int uu = 0; uu < U; ++uu)
+#pragma unroll
+            for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h[uu], x[uu][cc]);
+        }
+        for (; j < L; ++j) {
+          const double2 h = sv[j * kC];
+          const int li = sl[j * kC] * R;
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h, sVt[li + cc * LPR]);
         }
         if (p < a.n_loc) {
 #pragma unroll
@@ -552,10 +577,10 @@ __global__ void __launch_bounds__(kTiledThreads, 1) aug_spmmv_tiled(const SweepA
     if (lane < LPR) {
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) {
-        const int r = cc * LPR + lane;
-        red[warp * 3 * R + r] = d.ee[cc];
-        red[warp * 3 * R + R + r] = d.eor[cc];
-        red[warp * 3 * R + 2 * R + r] = d.eoi[cc];
+        const int r = cc * LPR + t;
+        red[g0 * 3 * R + r] = d.ee[cc];
+        red[g0 * 3 * R + R + r] = d.eor[cc];
+        red[g0 * 3 * R + 2 * R + r] = d.eoi[cc];
       }
     }
   }
@@ -563,14 +588,14 @@ __global__ void __launch_bounds__(kTiledThreads, 1) aug_spmmv_tiled(const SweepA
   for (int i = tid; i < 3 * R; i += kTiledThreads) {
     double sum = 0.0;
 #pragma unroll
-    for (int w = 0; w < NCW; ++w) sum += red[w * 3 * R + i];
+    for (int w = 0; w < NCWG; ++w) sum += red[w * 3 * R + i];
     a.partials[(int64_t)i * gridDim.x + blockIdx.x] = sum;
   }
 }
 
 enum Feed { kDirect = 0, kStaged = 1, kTiled = 2 };
 
-template <int R, int LPR, int U, int FEED>
+template <int R, int LPR, int U, int FEED, int CS = 1>
 struct Variant {
   static cudaError_t launch(bool init, const SweepArgs& a, int grid, cudaStream_t s) {
     if constexpr (FEED == kStaged) {
@@ -580,12 +605,12 @@ struct Variant {
         aug_spmmv_staged<R, LPR, U, false><<<grid, kThreads, kStagedSmem, s>>>(a);
     } else if constexpr (FEED == kTiled) {
       const int smem = a.tl.stages * a.tl.stage_bytes;
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (init)
-        aug_spmmv_tiled<R, LPR, U, true><<<grid, kTiledThreads, smem, s>>>(a);
+        aug_spmmv_tiled<R, LPR, U, CS, true><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
       else
-        aug_spmmv_tiled<R, LPR, U, false><<<grid, kTiledThreads, smem, s>>>(a);
+        aug_spmmv_tiled<R, LPR, U, CS, false><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
     } else {
       if (init)
         aug_spmmv_direct<R, LPR, U, true><<<grid, kThreads, 0, s>>>(a);
@@ -599,8 +624,9 @@ struct Variant {
     if constexpr (FEED == kStaged) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_staged<R, LPR, U, false>, kThreads, kStagedSmem);
     } else if constexpr (FEED == kTiled) {
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_tiled<R, LPR, U, false>, kTiledThreads, dyn_smem);
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_tiled<R, LPR, U, CS, false>, tiled_threads<LPR, CS>(),
+                                                    dyn_smem);
     } else {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_direct<R, LPR, U, false>, kThreads, 0);
     }
@@ -618,25 +644,29 @@ struct Entry {
   OccFn occ;
 };
 #define KPM_VARIANT(R, LPR, U, F, NAME) {R, NAME, F, Variant<R, LPR, U, F>::launch, Variant<R, LPR, U, F>::occupancy}
+#define KPM_VARIANT_CS(R, LPR, U, CS, NAME) \
+  {R, NAME, kTiled, Variant<R, LPR, U, kTiled, CS>::launch, Variant<R, LPR, U, kTiled, CS>::occupancy}
 // First entry of each width is the default (chosen from the B200 measurements in DESIGN.md).
 const Entry kTable[] = {
+    KPM_VARIANT(1, 1, 4, kTiled, "tiled.lpr1.u4"),
     KPM_VARIANT(1, 1, 4, kDirect, "direct.lpr1.u4"),
     KPM_VARIANT(1, 1, 8, kDirect, "direct.lpr1.u8"),
+    KPM_VARIANT(2, 2, 4, kTiled, "tiled.lpr2.u4"),
     KPM_VARIANT(2, 2, 4, kDirect, "direct.lpr2.u4"),
     KPM_VARIANT(2, 2, 8, kDirect, "direct.lpr2.u8"),
+    KPM_VARIANT(4, 4, 4, kTiled, "tiled.lpr4.u4"),
     KPM_VARIANT(4, 4, 4, kDirect, "direct.lpr4.u4"),
     KPM_VARIANT(4, 4, 8, kDirect, "direct.lpr4.u8"),
     KPM_VARIANT(8, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kStaged, "staged.lpr8.u4"),
-    KPM_VARIANT(8, 8, 8, kTiled, "tiled.lpr8.u8"),
     KPM_VARIANT(8, 8, 4, kDirect, "direct.lpr8.u4"),
     KPM_VARIANT(16, 8, 4, kTiled, "tiled.lpr8.u4"),
+    KPM_VARIANT_CS(16, 8, 4, 2, "tiled.lpr8.u4.cs2"),
     KPM_VARIANT(16, 16, 4, kTiled, "tiled.lpr16.u4"),
     KPM_VARIANT(16, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(16, 8, 4, kDirect, "direct.lpr8.u4"),
     KPM_VARIANT(32, 8, 4, kTiled, "tiled.lpr8.u4"),
-    KPM_VARIANT(32, 16, 4, kTiled, "tiled.lpr16.u4"),
-    KPM_VARIANT(32, 32, 4, kTiled, "tiled.lpr32.u4"),
+    KPM_VARIANT_CS(32, 8, 4, 2, "tiled.lpr8.u4.cs2"),
     KPM_VARIANT(32, 8, 2, kTiled, "tiled.lpr8.u2"),
     KPM_VARIANT(32, 16, 4, kStaged, "staged.lpr16.u4"),
     KPM_VARIANT(32, 8, 2, kDirect, "direct.lpr8.u2"),

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+P="python scripts/prof_run.py --lattice 200,100,40 --M 8"
+$P --R 32,16 > gpurun_out/p4_plain.log 2>&1 || exit 1
+cat gpurun_out/p4_plain.log
+ncu --set full --clock-control none --import-source on -k regex:aug_spmmv -s 1 -c 1 -o gpurun_out/prof_t32 $P --R 32 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:aug_spmmv -s 1 -c 1 -o gpurun_out/prof_t16 $P --R 16 > /dev/null 2>&1
+ls gpurun_out

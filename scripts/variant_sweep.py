@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--R", default="1,2,4,8,16,32")
     ap.add_argument("--M", type=int, default=40)
     ap.add_argument("--grid-per-sm", default="0")
+    ap.add_argument("--warm-seconds", type=float, default=0.0, help="run this long before timing (power-cap steady state)")
     args = ap.parse_args()
     import paper_1410_5242_b200 as kpm
 
@@ -34,7 +35,11 @@ def main():
                 os.environ["KPM_GRID_PER_SM"] = g
                 with kpm.KpmContext() as ctx:
                     ctx.set_matrix(rp, col, val, a, b)
+                    import time as _t
+                    t0 = _t.time()
                     ctx.moments(args.M, R, SEED, want_eta=False)
+                    while _t.time() - t0 < args.warm_seconds:
+                        ctx.moments(args.M, R, SEED, want_eta=False)
                     mu, _ = ctx.moments(args.M, R, SEED, want_eta=False)
                     name = ctx.last_kernel()
                     t, sw, ns = ctx.last_timing()
