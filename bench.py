@@ -181,8 +181,6 @@ def main():
         return run_reference(args, rank, world)
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    if world > 1:
-        raise SystemExit("multi-GPU bench not built yet")
 
     import torch
 
@@ -190,18 +188,49 @@ def main():
 
     torch.cuda.set_device(local)
     stream = torch.cuda.current_stream()
-    nx, ny, nz = (int(t) for t in args.lattice.split(","))
-    nx *= world
-    lat, rp, col, val, a, b = build_problem(nx, ny, nz)
-    n, nnz = lat.n, int(rp[-1])
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")  # plumbing only: NCCL id broadcast, barriers, max over ranks
+
+    def allmax(x):
+        if dist is None:
+            return x
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    # Bar weak scaling: x grows with the GPU count, each rank owns one C3-sized x-slab
+    px, ny, nz = (int(t) for t in args.lattice.split(","))
+    nx = px * world
+    lat = Lattice(nx, ny, nz)
+    x0, x1 = px * rank, px * (rank + 1)
+    rp, col, val = generate_csr(lat, x0, x1)
+    lo, hi = gershgorin(rp, col, val, row_begin=x0 * lat.rows_per_plane)
+    lo, hi = -allmax(-lo), allmax(hi)
+    a, b = scale_factors(lo, hi)
+    n, nnz = lat.n, lat.nnz_expected()
+    n_loc, nnz_loc = len(rp) - 1, int(rp[-1])
     M, R = args.M, args.R
-    ctx = kpm.KpmContext(device=local, cuda_stream=stream.cuda_stream)
-    ctx.set_matrix(rp, col, val, a, b)
+    uid = None
+    if world > 1:
+        box = [kpm.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        uid = box[0]
+    ctx = kpm.KpmContext(device=local, nranks=world, rank=rank, nccl_unique_id=uid, cuda_stream=stream.cuda_stream)
+    row_begin = x0 * lat.rows_per_plane
+    ctx.set_matrix(rp, col, val, a, b, n_global=n, row_begin=row_begin)
     n_blocks = (R + 31) // 32
 
     for _ in range(args.warmup):
         ctx.moments(M, R, SEED)
-    torch.cuda.synchronize()
+    barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sweep_ms = []
     with ClockSampler(local) as clk:
@@ -210,39 +239,40 @@ def main():
             mu, _ = ctx.moments(M, R, SEED, want_eta=False)
             sweep_ms.append(ctx.last_timing()[1])
         ev1.record(stream)
-        torch.cuda.synchronize()
+        barrier()
     clocks = clk.summary()
-    t_ms = ev0.elapsed_time(ev1)
+    t_ms = allmax(ev0.elapsed_time(ev1))
     flops_step = (M // 2) * alg_flops_per_sweep(n, nnz, R)
     value = args.steps * flops_step / (t_ms * 1e-3) / 1e9
     hbm, peak_src = peaks()
-    sweep = statistics.median(sweep_ms)
-    bytes_sweep = alg_bytes_per_sweep(n, nnz, R)
+    sweep = allmax(statistics.median(sweep_ms))
+    bytes_sweep = alg_bytes_per_sweep(n_loc, nnz_loc, R)  # per rank per launch
     achieved = bytes_sweep / (sweep * 1e-3) / 1e9
     bmin = alg_bytes_per_sweep(n, nnz, R) / alg_flops_per_sweep(n, nnz, R)
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
-        traffic = json.load(open(tf)).get(f"{nx}x{ny}x{nz}/R{R}")
+        traffic = json.load(open(tf)).get(f"{px}x{ny}x{nz}/R{R}")
     out = {
         "metric": "augmented SpMMV Gflop/s (cplx dbl)", "value": value, "unit": "Gflop/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"C3 TI lattice {nx}x{ny}x{nz} x 4 orbitals, M={M}, R={R}" if world == 1 else
-                   f"Bar TI lattice {nx}x{ny}x{nz}, M={M}, R={R}", "lattice": [nx, ny, nz], "N": n, "N_nz": nnz,
-                   "M": M, "R": R, "parallelism": f"x-slab dp{world}",
-                   "l2": "inputs larger than L2 (V, W %.2f GB each; matrix %.2f GB)" % (
-                       16 * R * n / 1e9, 20 * nnz / 1e9)},
+        "config": {"workload": (f"C3 TI lattice {nx}x{ny}x{nz} x 4 orbitals, M={M}, R={R}" if world == 1 else
+                                f"Bar TI lattice {nx}x{ny}x{nz} x 4 orbitals (C3 slab per GPU), M={M}, R={R}"),
+                   "lattice": [nx, ny, nz], "N": n, "N_nz": nnz, "M": M, "R": R, "parallelism": f"x-slab dp{world}",
+                   "kernel_variant": ctx.last_kernel(),
+                   "l2": "inputs larger than L2 (V, W %.2f GB each per GPU; matrix %.2f GB)" % (
+                       16 * R * n_loc / 1e9, 20 * nnz_loc / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "kernel": "aug_spmmv main sweep", "sweep_ms": sweep,
+                     "traffic": traffic, "kernel": "aug_spmmv main sweep (per GPU)", "sweep_ms": sweep,
                      "alg_bytes_per_launch": bytes_sweep, "peak_source": peak_src,
-                     "B_min_bytes_per_flop": bmin, "P_mem_gflops": hbm / bmin,
-                     "kernel_gflops": alg_flops_per_sweep(n, nnz, R) / (sweep * 1e-3) / 1e9},
-        "gpu_launches": args.steps * n_blocks * (M // 2 + 2),
+                     "B_min_bytes_per_flop": bmin, "P_mem_gflops_per_gpu": hbm / bmin,
+                     "kernel_gflops_per_gpu": alg_flops_per_sweep(n_loc, nnz_loc, R) / (sweep * 1e-3) / 1e9},
+        "gpu_launches": args.steps * n_blocks * ((M // 2) * (2 if world > 1 else 1) + 2),
         "clocks": clocks,
     }
     # R sweep of the same lattice (HBM -> cache bottleneck shift), shorter M
-    if not args.no_r_sweep:
+    if not args.no_r_sweep and world == 1:
         by_r = {}
         for r in (1, 2, 4, 8, 16, 32):
             ctx.moments(200, r, SEED, want_eta=False)
@@ -251,32 +281,35 @@ def main():
             bs = alg_bytes_per_sweep(n, nnz, r)
             by_r[str(r)] = {"sweep_ms": sw, "gflops": alg_flops_per_sweep(n, nnz, r) / (sw * 1e-3) / 1e9,
                             "hbm_gbs_alg": bs / (sw * 1e-3) / 1e9, "frac": bs / (sw * 1e-3) / 1e9 / hbm,
-                            "P_mem_gflops": hbm / (bs / alg_flops_per_sweep(n, nnz, r))}
+                            "P_mem_gflops": hbm / (bs / alg_flops_per_sweep(n, nnz, r)), "kernel": ctx.last_kernel()}
         out["by_R"] = by_r
     # e2e: host CSR in, mu/eta out, through the C ABI, copies inside the timed region
     if not args.no_e2e:
         h2d = rp.nbytes + col.nbytes + val.nbytes
         d2h = M * 8 + R * M * 16
-        torch.cuda.synchronize()
+        barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            ctx.set_matrix(rp, col, val, a, b)
+            ctx.set_matrix(rp, col, val, a, b, n_global=n, row_begin=row_begin)
             ctx.moments(M, R, SEED, want_eta=True)
         e1.record(stream)
-        torch.cuda.synchronize()
-        te = e0.elapsed_time(e1)
+        barrier()
+        te = allmax(e0.elapsed_time(e1))
         out["e2e"] = {"value": args.steps * flops_step / (te * 1e-3) / 1e9, "unit": "Gflop/s",
-                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                      "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
                       "ms_per_step": te / args.steps,
                       "note": "kpm_set_matrix(host CSR: validation, SELL build, H2D) + kpm_moments (D2H mu, eta)"}
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         gf, threads, sweeps, t = oracle_sample(rp, col, val, a, b, n, nnz)
         out["cpu_baseline"] = {"value": gf, "unit": "Gflop/s", "cores": threads, "kind": "oracle",
                                "sample": f"same lattice, 1 random vector, {sweeps} sweeps ({t:.1f} s)"}
     ctx.close()
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

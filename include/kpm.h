@@ -79,6 +79,10 @@ typedef struct {
   int mem;                      /* KPM_MEM_HOST or KPM_MEM_DEVICE (all three arrays)        */
 } kpm_csr;
 
+/* A fresh 128-byte NCCL unique id for kpm_options.nccl_unique_id (rank 0 calls it and
+ * broadcasts the bytes to the other ranks out of band, e.g. with torch.distributed). */
+kpm_status kpm_get_unique_id(void* out128);
+
 /* Create a context on opt->device.  nranks > 1: also creates the NCCL communicator
  * (collective).  *out is NULL on failure. */
 kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt);
@@ -135,6 +139,21 @@ kpm_status kpm_get_sell_info(const kpm_ctx* ctx, kpm_sell_info* info);
  * halo slot).  Any pointer may be NULL to skip that array. */
 kpm_status kpm_export_sell(const kpm_ctx* ctx, double* val, int32_t* col, int64_t* cptr,
                            int32_t* perm, int64_t* halo);
+
+/* Host-only planning of the halo exchange (no GPU needed; the same code kpm_set_matrix
+ * runs).  Row distribution: rank q owns global rows [row_begins[q], row_begins[q+1]).
+ * kpm_plan_recv: this rank's receive runs, from its CSR rows (row_ptr, global col) --
+ *   4 int64 per run: (owner rank, first global row, count, first halo slot).  Halo slots are
+ *   the distinct remote columns ordered by (owner, global id).  Call with runs = NULL to get
+ *   *n_runs; otherwise *n_runs is the capacity in runs.
+ * kpm_plan_send: the send runs answering the n_req (first global row, count) pairs `req`
+ *   that rank `peer` requested from this rank (rows [row_begin, row_end), sigma = 1) --
+ *   3 int64 per run: (peer, first local position, count).  KPM_ERANGE if a request is not
+ *   inside this rank's rows. */
+kpm_status kpm_plan_recv(int nranks, const int64_t* row_begins, int rank, const int64_t* row_ptr,
+                         const int64_t* col, int64_t* n_runs, int64_t* runs);
+kpm_status kpm_plan_send(int64_t row_begin, int64_t row_end, int peer, int64_t n_req, const int64_t* req,
+                         int64_t* n_runs, int64_t* runs);
 
 /* Human-readable description of the last error on ctx (or of the last kpm_create failure
  * when ctx is NULL).  Valid until the next call on ctx. */

@@ -20,8 +20,9 @@ STATUS_NAMES = ["KPM_OK", "KPM_EINVAL", "KPM_ESTATE", "KPM_ERANGE", "KPM_ENOMEM"
                 "KPM_EZERONORM", "KPM_WDIVERGED"]
 
 # exported symbols declared in include/kpm.h
-ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_export_sell", "kpm_get_sell_info", "kpm_last_error",
-               "kpm_last_kernel", "kpm_last_timing", "kpm_moments", "kpm_moments_v0", "kpm_set_matrix"]
+ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_export_sell", "kpm_get_sell_info", "kpm_get_unique_id",
+               "kpm_last_error", "kpm_last_kernel", "kpm_last_timing", "kpm_moments", "kpm_moments_v0",
+               "kpm_plan_recv", "kpm_plan_send", "kpm_set_matrix"]
 
 
 class KpmError(RuntimeError):
@@ -71,6 +72,9 @@ def load_library():
     lib.kpm_last_error.restype = ctypes.c_char_p
     lib.kpm_last_kernel.argtypes = [P]
     lib.kpm_last_kernel.restype = ctypes.c_char_p
+    lib.kpm_get_unique_id.argtypes = [P]
+    lib.kpm_plan_recv.argtypes = [i32, P, i32, P, P, P, P]
+    lib.kpm_plan_send.argtypes = [i64, i64, i32, i64, P, P, P]
     lib.kpm_destroy.argtypes = [P]
     lib.kpm_destroy.restype = None
     for name in ABI_SYMBOLS:
@@ -86,6 +90,45 @@ def _ptr(a):
     if isinstance(a, np.ndarray):
         return a.ctypes.data_as(ctypes.c_void_p)
     return ctypes.c_void_p(int(a.data_ptr()))  # torch tensor (device memory plumbing)
+
+
+def get_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0), to broadcast to the other ranks."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    st = lib.kpm_get_unique_id(buf)
+    if st != KPM_OK:
+        raise KpmError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def plan_recv(row_begins, rank, row_ptr, col):
+    """Receive runs (owner, first global row, count, first halo slot) -- host only."""
+    lib = load_library()
+    rb = np.ascontiguousarray(row_begins, dtype=np.int64)
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    c = np.ascontiguousarray(col, dtype=np.int64)
+    n = ctypes.c_int64(0)
+    st = lib.kpm_plan_recv(len(rb) - 1, _ptr(rb), rank, _ptr(rp), _ptr(c), ctypes.byref(n), None)
+    if st != KPM_OK:
+        raise KpmError(st, "kpm_plan_recv")
+    out = np.zeros((n.value, 4), dtype=np.int64)
+    st = lib.kpm_plan_recv(len(rb) - 1, _ptr(rb), rank, _ptr(rp), _ptr(c), ctypes.byref(n), _ptr(out))
+    if st != KPM_OK:
+        raise KpmError(st, "kpm_plan_recv")
+    return out
+
+
+def plan_send(row_begin, row_end, peer, req):
+    """Send runs (peer, first local position, count) answering `req` ((first, count) pairs)."""
+    lib = load_library()
+    rq = np.ascontiguousarray(req, dtype=np.int64).reshape(-1, 2)
+    n = ctypes.c_int64(len(rq))
+    out = np.zeros((max(len(rq), 1), 3), dtype=np.int64)
+    st = lib.kpm_plan_send(row_begin, row_end, peer, len(rq), _ptr(rq), ctypes.byref(n), _ptr(out))
+    if st != KPM_OK:
+        raise KpmError(st, "kpm_plan_send")
+    return out[: n.value]
 
 
 class KpmContext:

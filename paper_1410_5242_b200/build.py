@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libkpm.so")
-SOURCES = ["kernels.cu", "kpm_abi.cu", "sell_build.cpp"]
+SOURCES = ["kernels.cu", "kpm_abi.cu", "sell_build.cpp", "halo_plan.cpp", "plan_abi.cpp"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -18,6 +18,18 @@ def _nvcc() -> str:
         if cand == "nvcc" or os.path.exists(cand):
             return cand
     return "nvcc"
+
+
+def _nccl_dir() -> str:
+    """NCCL headers + library of the image (the pip nvidia-nccl package torch itself loads)."""
+    import importlib.util
+
+    spec = importlib.util.find_spec("nvidia")
+    for base in list(spec.submodule_search_locations or []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("nccl.h not found (expected site-packages/nvidia/nccl)")
 
 
 def _stale() -> bool:
@@ -32,9 +44,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
+    nccl = _nccl_dir()
     cmd = [_nvcc(), *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
-           "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}", "-o", tmp]
+           "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}", f"-I{nccl}/include", "-o", tmp]
     cmd += [os.path.join(CSRC, s) for s in SOURCES]
+    cmd += [f"-L{nccl}/lib", "-l:libnccl.so.2", f"-Xlinker=-rpath={nccl}/lib"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     with open(os.path.join(PKG, "build.log"), "w") as f:
         f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)

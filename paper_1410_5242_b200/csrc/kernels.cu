@@ -41,15 +41,15 @@ __device__ __forceinline__ double2 z4_phase(uint64_t seed, uint64_t row, uint32_
 }
 
 __global__ void z4_init_kernel(double2* __restrict__ V, double2* __restrict__ W, const int* __restrict__ perm,
-                               int64_t n_loc, int64_t n_total, int R, int64_t row_begin, int64_t col_begin,
-                               int r_valid, uint64_t seed) {
+                               int64_t n_loc, int64_t n_pad, const int64_t* __restrict__ halo_rows, int64_t n_total,
+                               int R, int64_t row_begin, int64_t col_begin, int r_valid, uint64_t seed) {
   const int64_t n_el = n_total * R;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = e / R;
     const int r = (int)(e - p * R);
     double2 v = make_double2(0.0, 0.0);
-    if (p < n_loc && r < r_valid) {
-      const int64_t row = row_begin + (perm ? (int64_t)perm[p] : p);
+    if (r < r_valid && (p < n_loc || p >= n_pad)) {
+      const int64_t row = p < n_loc ? row_begin + (perm ? (int64_t)perm[p] : p) : halo_rows[p - n_pad];
       v = z4_phase(seed, (uint64_t)row, (uint32_t)(col_begin + r));
     }
     V[e] = v;
@@ -167,8 +167,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+
+// i-th chunk of the launch's work list (a contiguous range, or a host-built list such as the
+// edge / interior chunks of the multi-GPU split).
+__device__ __forceinline__ int64_t chunk_at(const SweepArgs& a, int64_t i) {
+  return a.chunk_list ? __ldg(a.chunk_list + a.chunk_begin + i) : a.chunk_begin + i;
 }
 
 template <int R, int LPR, int U>
@@ -284,7 +287,7 @@ __device__ __forceinline__ void cta_reduce(const SweepArgs& a, Dots<R / LPR>& d,
     double s = 0.0;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) s += red[w * 3 * R + i];
-    a.partials[(int64_t)i * gridDim.x + blockIdx.x] = s;
+    a.partials[(int64_t)i * a.pstride + blockIdx.x] = s;
   }
 }
 
@@ -298,11 +301,12 @@ __global__ void __launch_bounds__(kThreads) aug_spmmv_direct(const SweepArgs a) 
   const uint64_t pol = policy_evict_first();
   Dots<Cf::CPL> d;
   d.zero();
-  const int64_t g0 = a.chunk_begin * (kC / RW), g1 = a.chunk_end * (kC / RW);
-  for (int64_t g = g0 + blockIdx.x * (int64_t)(kThreads / 32) + warp; g < g1; g += (int64_t)gridDim.x * (kThreads / 32)) {
-    const int64_t p = g * RW + q;
-    const int64_t c = (g * RW) >> 5;
-    const int k = (int)(p & 31);
+  constexpr int G = kC / RW;
+  const int64_t g1 = (a.chunk_end - a.chunk_begin) * G;
+  for (int64_t g = blockIdx.x * (int64_t)(kThreads / 32) + warp; g < g1; g += (int64_t)gridDim.x * (kThreads / 32)) {
+    const int64_t c = chunk_at(a, g / G);
+    const int k = (int)((g % G) * RW) + q;
+    const int64_t p = c * kC + k;
     const int64_t s0 = __ldg(a.cptr + c);
     const int L = (int)((__ldg(a.cptr + c + 1) - s0) >> 5);
     row_group<R, LPR, U, INIT, false>(a, a.val + s0 + k, a.col + s0 + k, L, p, t, pol, d);
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 2) aug_spmmv_staged(const SweepArgs 
 
   auto issue = [&](int64_t k) {  // producer: stage tile k (one elected thread)
     const int s = (int)(k % kStages);
-    const int64_t c = a.chunk_begin + blockIdx.x + k * gridDim.x;
+    const int64_t c = chunk_at(a, blockIdx.x + k * gridDim.x);
     const int64_t s0 = a.cptr[c];
     const int L = (int)((a.cptr[c + 1] - s0) >> 5);
     const uint32_t bar = smem_u32(&full[s]);
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 2) aug_spmmv_staged(const SweepArgs 
   d.zero();
   for (int64_t k = 0; k < my_tiles; ++k) {
     const int s = (int)(k % kStages);
-    const int64_t c = a.chunk_begin + blockIdx.x + k * gridDim.x;
+    const int64_t c = chunk_at(a, blockIdx.x + k * gridDim.x);
     const int L = (int)((__ldg(a.cptr + c + 1) - __ldg(a.cptr + c)) >> 5);
     mbar_wait(smem_u32(&full[s]), (uint32_t)((k / kStages) & 1));
     const double2* sv = reinterpret_cast<const double2*>(ring + s * kStageBytes);
@@ -403,15 +407,6 @@ __global__ void eta_finalize_kernel(const double* __restrict__ partials, int n_s
 constexpr int kMaxTileStages = 4;
 constexpr int kTileBudget = 232448 - 8192;  // minus static smem (reduction buffer, barriers)  // 227 KB dynamic shared memory minus margin
 
-__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int n = __shfl_up_sync(0xffffffffu, v, off);
-    if (lane >= off) v += n;
-  }
-  return v;
-}
-
 // CS = column split: CS consumer warps share a row group, each owning CPL/CS of the lane's
 // block columns (more warps in flight for the same registers; val/lcol reads repeat CS times).
 // Consumer warps per column part: one per row group of a chunk, at most 8 (so R < 8 uses
@@ -430,10 +425,10 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
   constexpr int NCWG = tiled_ncwg<LPR>(); // consumer warps per column part
   constexpr int NCW = NCWG * CS;          // consumer warps
   constexpr int kTiledThreads = tiled_threads<LPR, CS>();
-  constexpr int ROWB = R * 16;            // bytes per V/W row
   extern __shared__ __align__(128) unsigned char tsm[];
   __shared__ __align__(8) uint64_t full[kMaxTileStages], empty[kMaxTileStages];
   __shared__ int tile_len[kMaxTileStages];
+  __shared__ int64_t tile_chunk[kMaxTileStages];
   __shared__ double red[NCWG * 3 * R];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const TileLayout tl = a.tl;
@@ -457,14 +452,15 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
     // Lane i < 16 holds slot i of the chunk's copy record (header + up to 15 bulk copies);
     // the record of tile k+1 is loaded while tile k is issued, so no metadata load sits on
     // the producer's critical path.
-    auto load_rec = [&](int64_t k) -> uint4 {
-      const int64_t c = a.chunk_begin + blockIdx.x + k * gridDim.x;
-      return lane < 16 ? __ldg(a.rec + c * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
-    };
-    uint4 nxt = my_tiles > 0 ? load_rec(0) : make_uint4(0u, 0u, 0u, 0u);
+    int64_t c_nxt = my_tiles > 0 ? chunk_at(a, blockIdx.x) : 0;
+    uint4 nxt = my_tiles > 0 && lane < 16 ? __ldg(a.rec + c_nxt * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
     for (int64_t k = 0; k < my_tiles; ++k) {
       const uint4 cur = nxt;
-      if (k + 1 < my_tiles) nxt = load_rec(k + 1);
+      const int64_t c_cur = c_nxt;
+      if (k + 1 < my_tiles) {
+        c_nxt = chunk_at(a, blockIdx.x + (k + 1) * gridDim.x);
+        nxt = lane < 16 ? __ldg(a.rec + c_nxt * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
+      }
       const int s = (int)(k % tl.stages);
       const uint32_t total = __shfl_sync(0xffffffffu, INIT ? cur.y : cur.x, 0);
       const uint32_t L = __shfl_sync(0xffffffffu, cur.z, 0);
@@ -474,6 +470,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
       const uint32_t bar = smem_u32(&full[s]);
       if (lane == 0) {
         tile_len[s] = (int)L;
+        tile_chunk[s] = c_cur;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_expect_tx(bar, total);
       }
@@ -497,7 +494,6 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
     const int t = lane - q * LPR + part * CPL * LPR;  // first block column of this lane
     for (int64_t k = 0; k < my_tiles; ++k) {
       const int s = (int)(k % tl.stages);
-      const int64_t c = a.chunk_begin + blockIdx.x + k * gridDim.x;
       const unsigned char* st = tsm + (size_t)s * tl.stage_bytes;
       const double2* sV = reinterpret_cast<const double2*>(st);
       const double2* sW = reinterpret_cast<const double2*>(st + tl.off_w);
@@ -505,6 +501,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
       const uint16_t* slc = reinterpret_cast<const uint16_t*>(st + tl.off_lcol);
       mbar_wait(smem_u32(&full[s]), (uint32_t)((k / tl.stages) & 1));
       const int L = tile_len[s];
+      const int64_t c = tile_chunk[s];
       for (int gq = g0; gq < G; gq += NCWG) {
         const int kr = gq * RW + q;
         const int64_t p = c * kC + kr;
@@ -589,7 +586,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
     double sum = 0.0;
 #pragma unroll
     for (int w = 0; w < NCWG; ++w) sum += red[w * 3 * R + i];
-    a.partials[(int64_t)i * gridDim.x + blockIdx.x] = sum;
+    a.partials[(int64_t)i * a.pstride + blockIdx.x] = sum;
   }
 }
 
@@ -743,10 +740,11 @@ static int elementwise_grid(int64_t n_el) {
   return (int)g;
 }
 
-cudaError_t launch_z4_init(double2* V, double2* W, const int* perm, int64_t n_loc, int64_t n_rows_total, int R,
-                           int64_t row_begin, int64_t col_begin, int r_valid, uint64_t seed, cudaStream_t s) {
-  z4_init_kernel<<<elementwise_grid(n_rows_total * R), 256, 0, s>>>(V, W, perm, n_loc, n_rows_total, R, row_begin,
-                                                                     col_begin, r_valid, seed);
+cudaError_t launch_z4_init(double2* V, double2* W, const int* perm, int64_t n_loc, int64_t n_pad, const int64_t* halo_rows,
+                           int64_t n_rows_total, int R, int64_t row_begin, int64_t col_begin, int r_valid,
+                           uint64_t seed, cudaStream_t s) {
+  z4_init_kernel<<<elementwise_grid(n_rows_total * R), 256, 0, s>>>(V, W, perm, n_loc, n_pad, halo_rows, n_rows_total, R,
+                                                                     row_begin, col_begin, r_valid, seed);
   return cudaGetLastError();
 }
 
@@ -757,11 +755,11 @@ cudaError_t launch_v0_upload_permute(double2* V, double2* W, const double2* v0_d
   return cudaGetLastError();
 }
 
-cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int grid, double2* eta_even,
+cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int width, double2* eta_even,
                                 double2* eta_odd, cudaStream_t s) {
   const int64_t n_threads = (int64_t)n_sweeps * 3 * R * 32;
   const int blocks = (int)((n_threads + 255) / 256);
-  eta_finalize_kernel<<<blocks, 256, 0, s>>>(partials, n_sweeps, R, grid, eta_even, eta_odd);
+  eta_finalize_kernel<<<blocks, 256, 0, s>>>(partials, n_sweeps, R, width, eta_even, eta_odd);
   return cudaGetLastError();
 }
 

@@ -12,7 +12,10 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/kpm.h"
+#include "halo_plan.h"
 #include "kpm_internal.h"
 #include "sell_build.h"
 
@@ -53,11 +56,33 @@ struct kpm_ctx {
   size_t v0_cap = 0;
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+  // multi-rank (nranks > 1): row distribution, halo exchange plan, NCCL
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_edge = nullptr, ev_halo = nullptr;
+  std::vector<int64_t> row_begins;  // nranks+1
+  std::vector<RecvRun> recv_runs;
+  std::vector<SendRun> send_runs;
+  int64_t* edge_list = nullptr;     // device: chunks holding sent rows or reading halo slots
+  int64_t* interior_list = nullptr; // device: the other chunks
+  int64_t n_edge = 0, n_interior = 0;
+  int64_t* halo_rows = nullptr;     // device: global id of each halo slot
   double last_total_ms = 0.0, last_sweep_ms = 0.0;
   int last_n_sweeps = 0;
 };
 
 static std::string g_create_err;
+
+#define KPM_NCCL(call)                                                              \
+  do {                                                                              \
+    ncclResult_t r_ = (call);                                                       \
+    if (r_ != ncclSuccess) {                                                        \
+      ctx->err = std::string(#call) + ": " + ncclGetErrorString(r_);                \
+      ctx->sticky = true;                                                           \
+      return KPM_ENCCL;                                                             \
+    }                                                                               \
+  } while (0)
 
 #define KPM_CUDA(call)                                                              \
   do {                                                                              \
@@ -86,8 +111,8 @@ extern "C" kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt) {
     g_create_err = "opt is NULL";
     return KPM_EINVAL;
   }
-  if (opt->nranks != 1 || opt->rank != 0) {
-    g_create_err = "nranks > 1 requires the NCCL build (not in this library yet)";
+  if (opt->nranks < 1 || opt->rank < 0 || opt->rank >= opt->nranks || (opt->nranks > 1 && !opt->nccl_unique_id)) {
+    g_create_err = "bad nranks / rank / nccl_unique_id";
     return KPM_EINVAL;
   }
   const int C = opt->sell_C ? opt->sell_C : kC;
@@ -114,6 +139,22 @@ extern "C" kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt) {
     kpm_destroy(ctx);
     return KPM_ECUDA;
   }
+  if (opt->nranks > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, opt->nccl_unique_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, opt->nranks, id, opt->rank);
+    if (r == ncclSuccess) {
+      e = cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_edge, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming);
+    }
+    if (r != ncclSuccess || e != cudaSuccess) {
+      g_create_err = r != ncclSuccess ? std::string("NCCL: ") + ncclGetErrorString(r)
+                                      : std::string("CUDA: ") + cudaGetErrorString(e);
+      kpm_destroy(ctx);
+      return r != ncclSuccess ? KPM_ENCCL : KPM_ECUDA;
+    }
+  }
   ctx->variant_override = env_int("KPM_VARIANT", -1);
   ctx->grid_per_sm = std::max(0, env_int("KPM_GRID_PER_SM", 0));
   ctx->tile_stages = std::max(0, env_int("KPM_TILE_STAGES", 0));
@@ -137,8 +178,37 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   if (ctx->h_eta) cudaFreeHost(ctx->h_eta);
   for (int i = 0; i < 4; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  cudaFree(ctx->edge_list);
+  cudaFree(ctx->interior_list);
+  cudaFree(ctx->halo_rows);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  if (ctx->ev_edge) cudaEventDestroy(ctx->ev_edge);
+  if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
+}
+
+extern "C" kpm_status kpm_get_unique_id(void* out) {
+  if (!out) return KPM_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return KPM_ENCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return KPM_OK;
+}
+
+// Small host<->device collective helpers for the setup (synchronous, compute stream).
+static kpm_status allgather_i64(kpm_ctx* ctx, const std::vector<int64_t>& mine, std::vector<int64_t>& all) {
+  const size_t n = mine.size(), P = (size_t)ctx->opt.nranks;
+  int64_t* d = nullptr;
+  KPM_CUDA(cudaMalloc(&d, sizeof(int64_t) * n * (P + 1)));
+  KPM_CUDA(cudaMemcpy(d, mine.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+  KPM_NCCL(ncclAllGather(d, d + n, n, ncclInt64, ctx->comm, ctx->stream));
+  all.resize(n * P);
+  KPM_CUDA(cudaMemcpyAsync(all.data(), d + n, sizeof(int64_t) * n * P, cudaMemcpyDeviceToHost, ctx->stream));
+  KPM_CUDA(cudaStreamSynchronize(ctx->stream));
+  KPM_CUDA(cudaFree(d));
+  return KPM_OK;
 }
 
 extern "C" const char* kpm_last_error(const kpm_ctx* ctx) {
@@ -155,6 +225,85 @@ static void free_sell(DevSell& s) {
   s = DevSell();
 }
 
+// Halo exchange plan (collective): receive runs from the halo list, requests to the owners,
+// send runs from the requests, edge / interior chunk split (halo_plan.h).
+static kpm_status plan_exchange(kpm_ctx* ctx, const HostSell& hs) {
+  const int P = ctx->opt.nranks, me = ctx->opt.rank;
+  const int64_t row_begin = ctx->row_begins[me], row_end = ctx->row_begins[me + 1];
+  ctx->recv_runs = plan_recv_runs(hs.halo, ctx->row_begins);
+  // requests: per owner q the (gfirst, count) pairs, in slot order
+  std::vector<std::vector<int64_t>> req(P);
+  for (const RecvRun& r : ctx->recv_runs) {
+    req[r.peer].push_back(r.gfirst);
+    req[r.peer].push_back(r.count);
+  }
+  std::vector<int64_t> counts(P), all;
+  for (int q = 0; q < P; ++q) counts[q] = (int64_t)req[q].size();
+  kpm_status st = allgather_i64(ctx, counts, all);  // all[p*P + q] = #int64 p requests from q
+  if (st != KPM_OK) return st;
+  int64_t tot_out = 0, tot_in = 0;
+  for (int q = 0; q < P; ++q) tot_out += all[(size_t)me * P + q];
+  for (int p = 0; p < P; ++p) tot_in += all[(size_t)p * P + me];
+  int64_t* dbuf = nullptr;
+  KPM_CUDA(cudaMalloc(&dbuf, sizeof(int64_t) * std::max<int64_t>(1, tot_out + tot_in)));
+  std::vector<int64_t> flat;
+  for (int q = 0; q < P; ++q) flat.insert(flat.end(), req[q].begin(), req[q].end());
+  if (tot_out) KPM_CUDA(cudaMemcpy(dbuf, flat.data(), sizeof(int64_t) * tot_out, cudaMemcpyHostToDevice));
+  KPM_NCCL(ncclGroupStart());
+  int64_t o = 0, in = tot_out;
+  for (int q = 0; q < P; ++q) {
+    const int64_t n = all[(size_t)me * P + q];
+    if (n) KPM_NCCL(ncclSend(dbuf + o, n, ncclInt64, q, ctx->comm, ctx->stream));
+    o += n;
+  }
+  for (int p = 0; p < P; ++p) {
+    const int64_t n = all[(size_t)p * P + me];
+    if (n) KPM_NCCL(ncclRecv(dbuf + in, n, ncclInt64, p, ctx->comm, ctx->stream));
+    in += n;
+  }
+  KPM_NCCL(ncclGroupEnd());
+  std::vector<int64_t> incoming(tot_in);
+  if (tot_in)
+    KPM_CUDA(cudaMemcpyAsync(incoming.data(), dbuf + tot_out, sizeof(int64_t) * tot_in, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  KPM_CUDA(cudaStreamSynchronize(ctx->stream));
+  KPM_CUDA(cudaFree(dbuf));
+  int64_t off = 0;
+  for (int p = 0; p < P; ++p) {
+    const int64_t n = all[(size_t)p * P + me];
+    std::vector<int64_t> rq(incoming.begin() + off, incoming.begin() + off + n);
+    off += n;
+    if (!plan_send_runs(p, rq, row_begin, row_end, hs.perm, ctx->send_runs))
+      return fail(ctx, KPM_EINVAL, "halo request does not map to contiguous local rows");
+  }
+  std::vector<int64_t> edge, interior;
+  plan_edge_chunks(hs.cptr, hs.col, hs.n_pad, hs.C, ctx->send_runs, edge, interior);
+  ctx->n_edge = (int64_t)edge.size();
+  ctx->n_interior = (int64_t)interior.size();
+  KPM_CUDA(cudaMalloc(&ctx->edge_list, sizeof(int64_t) * std::max<size_t>(1, edge.size())));
+  KPM_CUDA(cudaMalloc(&ctx->interior_list, sizeof(int64_t) * std::max<size_t>(1, interior.size())));
+  KPM_CUDA(cudaMalloc(&ctx->halo_rows, sizeof(int64_t) * std::max<size_t>(1, hs.halo.size())));
+  if (!edge.empty())
+    KPM_CUDA(cudaMemcpy(ctx->edge_list, edge.data(), sizeof(int64_t) * edge.size(), cudaMemcpyHostToDevice));
+  if (!interior.empty())
+    KPM_CUDA(cudaMemcpy(ctx->interior_list, interior.data(), sizeof(int64_t) * interior.size(), cudaMemcpyHostToDevice));
+  if (!hs.halo.empty())
+    KPM_CUDA(cudaMemcpy(ctx->halo_rows, hs.halo.data(), sizeof(int64_t) * hs.halo.size(), cudaMemcpyHostToDevice));
+  return KPM_OK;
+}
+
+// After a sweep: owners' new rows of X -> the neighbours' halo slots of X (grouped NCCL P2P).
+static kpm_status exchange_halo(kpm_ctx* ctx, double2* X, int Rk, cudaStream_t s) {
+  const int64_t n_pad = ctx->sell.n_pad;
+  KPM_NCCL(ncclGroupStart());
+  for (const SendRun& r : ctx->send_runs)
+    KPM_NCCL(ncclSend(X + r.pos * Rk, (size_t)r.count * Rk * 2, ncclDouble, r.peer, ctx->comm, s));
+  for (const RecvRun& r : ctx->recv_runs)
+    KPM_NCCL(ncclRecv(X + (n_pad + r.slot) * Rk, (size_t)r.count * Rk * 2, ncclDouble, r.peer, ctx->comm, s));
+  KPM_NCCL(ncclGroupEnd());
+  return KPM_OK;
+}
+
 extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, double b) {
   if (!ctx) return KPM_EINVAL;
   if (ctx->sticky) return fail(ctx, KPM_ESTATE, "context has a sticky CUDA/NCCL error: " + ctx->err);
@@ -167,6 +316,20 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
   if (ctx->opt.nranks == 1 && (H->row_begin != 0 || H->row_end != H->n_global))
     return fail(ctx, KPM_EINVAL, "single rank must own all rows");
   KPM_CUDA(cudaSetDevice(ctx->opt.device));
+  std::vector<int64_t> row_begins{0, H->n_global};
+  if (ctx->opt.nranks > 1) {  // collective: every rank's row range, must tile [0, n_global) in rank order
+    if (ctx->opt.sell_sigma != 1) return fail(ctx, KPM_EINVAL, "nranks > 1 needs sell_sigma = 1");
+    std::vector<int64_t> all;
+    kpm_status st0 = allgather_i64(ctx, {H->row_begin, H->row_end, H->n_global}, all);
+    if (st0 != KPM_OK) return st0;
+    row_begins.assign(1, 0);
+    for (int q = 0; q < ctx->opt.nranks; ++q) {
+      if (all[3 * q] != row_begins.back() || all[3 * q + 2] != H->n_global)
+        return fail(ctx, KPM_EINVAL, "row ranges do not tile [0, n_global) in rank order");
+      row_begins.push_back(all[3 * q + 1]);
+    }
+    if (row_begins.back() != H->n_global) return fail(ctx, KPM_EINVAL, "row ranges do not cover n_global");
+  }
 
   // host views of the CSR (device input is staged through the host for the build)
   std::vector<int64_t> rp_h, col_h;
@@ -202,6 +365,7 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
                            berr);
   if (st) return fail(ctx, (kpm_status)st, berr);
   if (ctx->opt.nranks == 1 && hs.n_halo != 0) return fail(ctx, KPM_EINVAL, "internal: halo on a single rank");
+  ctx->row_begins = row_begins;
 
   // upload
   free_sell(ctx->sell);
@@ -248,6 +412,19 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
     std::vector<uint16_t>().swap(ctx->tiles.lcol);  // host copy no longer needed
   }
   ctx->halo = hs.halo;
+  ctx->row_begins = row_begins;
+  ctx->recv_runs.clear();
+  ctx->send_runs.clear();
+  cudaFree(ctx->edge_list);
+  cudaFree(ctx->interior_list);
+  cudaFree(ctx->halo_rows);
+  ctx->edge_list = ctx->interior_list = ctx->halo_rows = nullptr;
+  ctx->n_edge = 0;
+  ctx->n_interior = d.n_chunks;
+  if (ctx->opt.nranks > 1) {
+    kpm_status st1 = plan_exchange(ctx, hs);
+    if (st1 != KPM_OK) return st1;
+  }
   ctx->n_global = H->n_global;
   ctx->row_begin = H->row_begin;
   ctx->row_end = H->row_end;
@@ -321,7 +498,9 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   const int dyn_smem = variant_tiled(Rk, variant) ? tl.stages * tl.stage_bytes : 0;
   const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, sweep_occupancy(Rk, variant, dyn_smem));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * occ, s.n_chunks));
-  const size_t per_sweep = (size_t)3 * Rk * grid;
+  const bool multi = ctx->opt.nranks > 1;
+  const int parts = multi ? 2 : 1;  // edge + interior launches per sweep
+  const size_t per_sweep = (size_t)3 * Rk * grid * parts;
   if ((st = ensure(ctx, (void**)&ctx->partials, &ctx->partials_cap, per_sweep * n_sweeps, sizeof(double))) != KPM_OK)
     return st;
   size_t ecap = ctx->eta_cap;
@@ -349,39 +528,70 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     ctx->v0_cap = vcap;
     KPM_CUDA(cudaMemcpyAsync(ctx->v0_dev, v0, sizeof(double2) * s.n_loc * rb, cudaMemcpyHostToDevice, str));
     KPM_CUDA(launch_v0_upload_permute(ctx->X0, ctx->X1, ctx->v0_dev, s.perm, s.n_loc, n_rows_total, Rk, rb, str));
-  } else {
-    KPM_CUDA(launch_z4_init(ctx->X0, ctx->X1, s.perm, s.n_loc, n_rows_total, Rk, ctx->row_begin, col_begin, rb, seed,
-                            str));
+    if (multi && (st = exchange_halo(ctx, ctx->X0, Rk, str)) != KPM_OK) return st;
+  } else {  // halo slots get their Z4 values directly from their global ids: no exchange for nu_0
+    KPM_CUDA(launch_z4_init(ctx->X0, ctx->X1, s.perm, s.n_loc, s.n_pad, ctx->halo_rows, n_rows_total, Rk,
+                            ctx->row_begin, col_begin, rb, seed, str));
   }
   SweepArgs sa;
   sa.val = s.val;
   sa.col = s.col;
   sa.cptr = s.cptr;
   sa.n_loc = s.n_loc;
+  sa.chunk_list = nullptr;
   sa.chunk_begin = 0;
   sa.chunk_end = s.n_chunks;
   sa.rec = s.rec[lg];
   sa.lcol = s.lcol;
   sa.tl = tl;
   sa.b = ctx->b;
-  // a2: init sweep  W = a(H - b)V, eta_0, eta_1
-  sa.V = ctx->X0;
-  sa.W = ctx->X1;
-  sa.scale = ctx->a;
-  sa.partials = ctx->partials;
-  KPM_CUDA(launch_aug_spmmv(Rk, variant, true, sa, grid, str));
-  // a3: main sweeps  W <- 2a(H - b)V - W, eta_2m, eta_2m+1
-  KPM_CUDA(cudaEventRecord(ctx->ev[1], str));
-  sa.scale = 2.0 * ctx->a;
-  for (int m = 1; m < n_sweeps; ++m) {
+  sa.pstride = (int64_t)grid * parts;
+  // One sweep m (m = 0: init sweep W = a(H - b)V; m >= 1: W <- 2a(H - b)V - W), with the
+  // fused eta_2m, eta_2m+1 partials.  Multi-rank: edge chunks first, then the new boundary
+  // rows go to the neighbours on the comm stream while the interior chunks run (a5).
+  auto sweep = [&](int m) -> kpm_status {
+    const bool init = (m == 0);
     sa.V = (m & 1) ? ctx->X1 : ctx->X0;
     sa.W = (m & 1) ? ctx->X0 : ctx->X1;
-    sa.partials = ctx->partials + per_sweep * m;
-    KPM_CUDA(launch_aug_spmmv(Rk, variant, false, sa, grid, str));
-  }
+    sa.scale = init ? ctx->a : 2.0 * ctx->a;
+    double* part = ctx->partials + per_sweep * m;
+    if (!multi) {
+      sa.partials = part;
+      KPM_CUDA(launch_aug_spmmv(Rk, variant, init, sa, grid, str));
+      return KPM_OK;
+    }
+    if (m > 0) KPM_CUDA(cudaStreamWaitEvent(str, ctx->ev_halo, 0));  // V's halo slots have arrived
+    sa.chunk_list = ctx->edge_list;
+    sa.chunk_begin = 0;
+    sa.chunk_end = ctx->n_edge;
+    sa.partials = part;
+    KPM_CUDA(launch_aug_spmmv(Rk, variant, init, sa, grid, str));
+    if (m + 1 < n_sweeps) {
+      KPM_CUDA(cudaEventRecord(ctx->ev_edge, str));
+      KPM_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_edge, 0));
+      kpm_status est = exchange_halo(ctx, sa.W, Rk, ctx->comm_stream);
+      if (est != KPM_OK) return est;
+      KPM_CUDA(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
+    }
+    sa.chunk_list = ctx->interior_list;
+    sa.chunk_end = ctx->n_interior;
+    sa.partials = part + grid;
+    KPM_CUDA(launch_aug_spmmv(Rk, variant, init, sa, grid, str));
+    return KPM_OK;
+  };
+  // a2: init sweep, eta_0, eta_1
+  if ((st = sweep(0)) != KPM_OK) return st;
+  // a3: main sweeps, eta_2m, eta_2m+1
+  KPM_CUDA(cudaEventRecord(ctx->ev[1], str));
+  for (int m = 1; m < n_sweeps; ++m)
+    if ((st = sweep(m)) != KPM_OK) return st;
   KPM_CUDA(cudaEventRecord(ctx->ev[2], str));
   // a4: deterministic grid reduction of all sweeps' partials
-  KPM_CUDA(launch_eta_finalize(ctx->partials, n_sweeps, Rk, grid, ctx->eta_even, ctx->eta_odd, str));
+  KPM_CUDA(launch_eta_finalize(ctx->partials, n_sweeps, Rk, grid * parts, ctx->eta_even, ctx->eta_odd, str));
+  if (multi) {  // a6: the single global reduction, once, at the end (Table III)
+    KPM_NCCL(ncclAllReduce(ctx->eta_even, ctx->eta_even, (size_t)n_sweeps * Rk * 2, ncclDouble, ncclSum, ctx->comm, str));
+    KPM_NCCL(ncclAllReduce(ctx->eta_odd, ctx->eta_odd, (size_t)n_sweeps * Rk * 2, ncclDouble, ncclSum, ctx->comm, str));
+  }
   KPM_CUDA(cudaMemcpyAsync(ctx->h_eta, ctx->eta_even, sizeof(double2) * n_sweeps * Rk, cudaMemcpyDeviceToHost, str));
   KPM_CUDA(cudaMemcpyAsync(ctx->h_eta + ctx->eta_cap, ctx->eta_odd, sizeof(double2) * n_sweeps * Rk,
                            cudaMemcpyDeviceToHost, str));

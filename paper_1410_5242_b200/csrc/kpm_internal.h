@@ -44,10 +44,12 @@ struct SweepArgs {
   const double2* V;    // nu_m   (read only)
   double2* W;          // nu_{m-1} in, nu_{m+1} out
   int64_t n_loc;
-  int64_t chunk_begin, chunk_end;  // SELL chunks swept by this launch
+  const int64_t* chunk_list;       // NULL: chunks [chunk_begin, chunk_end); else chunk_list[chunk_begin .. chunk_end)
+  int64_t chunk_begin, chunk_end;
   double scale;        // 2a for the main sweep, a for the init sweep
   double b;
-  double* partials;    // [3R][gridDim]: per-CTA (eta_even, Re eta_odd, Im eta_odd) of this sweep
+  double* partials;    // [3R][pstride]: per-CTA (eta_even, Re eta_odd, Im eta_odd) of this launch at [i*pstride + cta]
+  int64_t pstride;
   // tiled feed only
   const uint4* rec;      // kRecSlots per chunk (sell_build.h)
   const uint16_t* lcol;
@@ -55,9 +57,11 @@ struct SweepArgs {
 };
 
 // Launch helpers (kernels.cu).  All return cudaGetLastError() of the launch.
-cudaError_t launch_z4_init(double2* V, double2* W, const int* perm, int64_t n_loc, int64_t n_rows_total,
-                           int R, int64_t row_begin, int64_t col_begin, int r_valid, uint64_t seed,
-                           cudaStream_t s);
+// V = Z4 start block for the local rows (global row row_begin + perm[p]) and the halo slots
+// (global row halo_rows[h], h = p - n_pad); padding rows and W = 0.
+cudaError_t launch_z4_init(double2* V, double2* W, const int* perm, int64_t n_loc, int64_t n_pad, const int64_t* halo_rows,
+                           int64_t n_rows_total, int R, int64_t row_begin, int64_t col_begin, int r_valid,
+                           uint64_t seed, cudaStream_t s);
 cudaError_t launch_v0_upload_permute(double2* V, double2* W, const double2* v0_dev, const int* perm,
                                      int64_t n_loc, int64_t n_rows_total, int R, int r_valid,
                                      cudaStream_t s);
@@ -71,8 +75,8 @@ bool variant_tiled(int R, int variant);
 // Shared-memory plan of the tiled feed for block width R, or stages == 0 if it does not fit.
 TileLayout plan_tiles(int R, int64_t max_other, int64_t max_width, int stages);  // stages 0 = default
 cudaError_t launch_aug_spmmv(int R, int variant, bool init, const SweepArgs& a, int grid, cudaStream_t s);
-// eta[m][r] (double2) for m in [0, n_sweeps) from partials[m][3R][grid]
-cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int grid, double2* eta_even,
+// eta[m][r] (double2) for m in [0, n_sweeps) from partials[m][3R][width] (width = launches x grid)
+cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int width, double2* eta_even,
                                 double2* eta_odd, cudaStream_t s);
 
 }  // namespace kpm
