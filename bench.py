@@ -223,7 +223,16 @@ def main():
         box = [kpm.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
         uid = box[0]
-    ctx = kpm.KpmContext(device=local, nranks=world, rank=rank, nccl_unique_id=uid, cuda_stream=stream.cuda_stream)
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
+    saved = os.dup(1)
+    os.dup2(2, 1)  # anything the native libraries print during setup goes to stderr
+    try:
+        ctx = kpm.KpmContext(device=local, nranks=world, rank=rank, nccl_unique_id=uid,
+                             cuda_stream=stream.cuda_stream)
+    finally:
+        os.dup2(saved, 1)
+        os.close(saved)
     row_begin = x0 * lat.rows_per_plane
     ctx.set_matrix(rp, col, val, a, b, n_global=n, row_begin=row_begin)
     n_blocks = (R + 31) // 32
