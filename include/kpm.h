@@ -155,6 +155,20 @@ kpm_status kpm_plan_recv(int nranks, const int64_t* row_begins, int rank, const 
 kpm_status kpm_plan_send(int64_t row_begin, int64_t row_end, int peer, int64_t n_req, const int64_t* req,
                          int64_t* n_runs, int64_t* runs);
 
+/* Density of states from the moments (north_star item 5; Eq. (2) `DOS`; the
+ * "second computationally inexpensive step" of P:258-260).  Host only, no context.
+ *   mu        M moments mu_n = tr T_n(H~) as returned by kpm_moments (mu_0 = N).
+ *   a, b      the rescaling H~ = a(H - b), a > 0.
+ *   energies  K energies of H (host), or NULL for the K Chebyshev nodes x_k = cos(pi(k+1/2)/K)
+ *             mapped to E = x/a + b.
+ *   kernel    KPM_KERNEL_JACKSON (damping g_n of the KPM review [Weisse06] cited at P:78) or
+ *             KPM_KERNEL_NONE (g_n = 1).
+ *   E_out, rho_out  K doubles each: rho(E) = a [g_0 mu_0 + 2 sum g_n mu_n T_n(x)] / (pi sqrt(1-x^2)),
+ *             x = a(E - b); 0 where |x| >= 1.  Integrates to mu_0 = N. */
+enum { KPM_KERNEL_NONE = 0, KPM_KERNEL_JACKSON = 1 };
+kpm_status kpm_dos(int M, const double* mu, double a, double b, int K, const double* energies, int kernel,
+                   double* E_out, double* rho_out);
+
 /* Human-readable description of the last error on ctx (or of the last kpm_create failure
  * when ctx is NULL).  Valid until the next call on ctx. */
 const char* kpm_last_error(const kpm_ctx* ctx);

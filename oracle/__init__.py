@@ -127,3 +127,42 @@ def eta_to_mu(eta: np.ndarray):
 
 def max_threads() -> int:
     return int(_load().ora_max_threads())
+
+
+# ---------------------------------------------------------------- DOS (NEXT #1) ----
+def jackson(M: int) -> np.ndarray:
+    """Jackson kernel g_n, n = 0..M-1 (Weisse et al., Rev. Mod. Phys. 78, 275 (2006) -- the
+    KPM review the paper cites as [Weisse06]):
+        g_n = [(M - n + 1) cos(pi n/(M+1)) + sin(pi n/(M+1)) cot(pi/(M+1))] / (M+1)."""
+    n = np.arange(M, dtype=np.float64)
+    q = np.pi / (M + 1)
+    return ((M - n + 1) * np.cos(q * n) + np.sin(q * n) / np.tan(q)) / (M + 1)
+
+
+def chebyshev_nodes(K: int) -> np.ndarray:
+    """x_k = cos(pi (k + 1/2) / K), k = 0..K-1."""
+    return np.cos(np.pi * (np.arange(K) + 0.5) / K)
+
+
+def dos(mu, a, b, K=None, energies=None, kernel="jackson"):
+    """Density of states rho(E) of H from mu_n = tr T_n(H~) (Eq. (2) `DOS`; the
+    reconstruction step of P:258-260):
+        rho~(x) = [g_0 mu_0 + 2 sum_{n>=1} g_n mu_n T_n(x)] / (pi sqrt(1 - x^2)),
+        E = x/a + b,  rho(E) = a rho~(a (E - b)).
+    Evaluated at `energies`, or at the K Chebyshev nodes.  Returns (E, rho)."""
+    mu = np.asarray(mu, dtype=np.float64)
+    M = len(mu)
+    g = jackson(M) if kernel == "jackson" else np.ones(M)
+    if energies is None:
+        x = chebyshev_nodes(K if K else 2 * M)
+    else:
+        x = a * (np.asarray(energies, dtype=np.float64) - b)
+    t_prev, t = np.ones_like(x), x.copy()
+    s = g[0] * mu[0] * t_prev
+    if M > 1:
+        s = s + 2.0 * g[1] * mu[1] * t
+    for n in range(2, M):  # T_n by the three-term recurrence
+        t_prev, t = t, 2.0 * x * t - t_prev
+        s = s + 2.0 * g[n] * mu[n] * t
+    rho_x = s / (np.pi * np.sqrt(1.0 - x * x))
+    return x / a + b, a * rho_x

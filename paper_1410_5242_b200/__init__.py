@@ -20,7 +20,7 @@ STATUS_NAMES = ["KPM_OK", "KPM_EINVAL", "KPM_ESTATE", "KPM_ERANGE", "KPM_ENOMEM"
                 "KPM_EZERONORM", "KPM_WDIVERGED"]
 
 # exported symbols declared in include/kpm.h
-ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_export_sell", "kpm_get_sell_info", "kpm_get_unique_id",
+ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_dos", "kpm_export_sell", "kpm_get_sell_info", "kpm_get_unique_id",
                "kpm_last_error", "kpm_last_kernel", "kpm_last_timing", "kpm_moments", "kpm_moments_v0",
                "kpm_plan_recv", "kpm_plan_send", "kpm_set_matrix"]
 
@@ -73,6 +73,7 @@ def load_library():
     lib.kpm_last_kernel.argtypes = [P]
     lib.kpm_last_kernel.restype = ctypes.c_char_p
     lib.kpm_get_unique_id.argtypes = [P]
+    lib.kpm_dos.argtypes = [i32, P, dbl, dbl, i32, P, i32, P, P]
     lib.kpm_plan_recv.argtypes = [i32, P, i32, P, P, P, P]
     lib.kpm_plan_send.argtypes = [i64, i64, i32, i64, P, P, P]
     lib.kpm_destroy.argtypes = [P]
@@ -100,6 +101,26 @@ def get_unique_id() -> bytes:
     if st != KPM_OK:
         raise KpmError(st, "ncclGetUniqueId failed")
     return buf.raw
+
+
+KPM_KERNEL_NONE, KPM_KERNEL_JACKSON = 0, 1
+
+
+def dos(mu, a, b, K=None, energies=None, kernel="jackson"):
+    """kpm_dos: (E, rho) from the moments (Jackson kernel by default)."""
+    lib = load_library()
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    if energies is not None:
+        energies = np.ascontiguousarray(energies, dtype=np.float64)
+        K = len(energies)
+    K = K or 2 * len(mu)
+    E = np.zeros(K)
+    rho = np.zeros(K)
+    kern = KPM_KERNEL_JACKSON if kernel == "jackson" else KPM_KERNEL_NONE
+    st = lib.kpm_dos(len(mu), _ptr(mu), float(a), float(b), K, _ptr(energies), kern, _ptr(E), _ptr(rho))
+    if st != KPM_OK:
+        raise KpmError(st, "kpm_dos")
+    return E, rho
 
 
 def plan_recv(row_begins, rank, row_ptr, col):

@@ -188,3 +188,18 @@ def test_c3_sampled_columns(pkg):
         eta_o = oracle.kpm_eta(rp, col, val, a, b, M, 1, SEED, col_begin=c)
         check(eta[c : c + 1], None, eta_o, cols=[0])
     assert mu[0] == lat.n and np.all(np.abs(mu) <= mu[0])
+
+
+def test_dos_pipeline_c1(pkg):
+    """GPU moments -> library Jackson DOS == oracle moments -> oracle DOS; integrates to N."""
+    lat, rp, col, val, a, b = problem((8, 8, 8))
+    M, R = 256, 16
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, _ = ctx.moments(M, R, SEED)
+    mu_o, _ = oracle.eta_to_mu(oracle.kpm_eta(rp, col, val, a, b, M, R, SEED))
+    E, rho = pkg.dos(mu, a, b, K=1024)
+    E_o, rho_o = oracle.dos(mu_o, a, b, K=1024)
+    assert np.max(np.abs(rho - rho_o)) <= 1e-10 * np.max(rho_o)
+    x = a * (E - b)
+    assert np.pi / len(x) * np.sum(rho / a * np.sqrt(1 - x * x)) == pytest.approx(lat.n, rel=1e-12)
