@@ -416,7 +416,9 @@ __host__ __device__ constexpr int tiled_ncwg() { return LPR < 8 ? LPR : 8; }
 template <int LPR, int CS>
 __host__ __device__ constexpr int tiled_threads() { return 32 * (tiled_ncwg<LPR>() * CS + 1); }
 
-template <int R, int LPR, int U, int CS, bool INIT>
+// WS: the old W rows travel in the tile (TMA) or, WS = false, straight into registers (LDG,
+// streaming) -- a smaller stage, so more CTAs fit per SM.
+template <int R, int LPR, int U, int CS, bool WS, bool INIT>
 __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(const SweepArgs a) {
   using Cf = Cfg<R, LPR, U>;
   constexpr int RW = Cf::RW, G = kC / RW;
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
         nxt = lane < 16 ? __ldg(a.rec + c_nxt * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
       }
       const int s = (int)(k % tl.stages);
-      const uint32_t total = __shfl_sync(0xffffffffu, INIT ? cur.y : cur.x, 0);
+      const uint32_t total = __shfl_sync(0xffffffffu, (INIT || !WS) ? cur.y : cur.x, 0);
       const uint32_t L = __shfl_sync(0xffffffffu, cur.z, 0);
       const uint32_t ncmd = __shfl_sync(0xffffffffu, cur.w, 0);
       if (k >= tl.stages) mbar_wait(smem_u32(&empty[s]), (uint32_t)(((k / tl.stages) - 1) & 1));
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
       if (lane >= 1 && (uint32_t)lane <= ncmd) {
         const uint32_t base = cur.w >> 28, bytes = cur.w & 0x0FFFFFFFu;
         const int64_t off = (int64_t)(((uint64_t)cur.y << 32) | cur.x);
-        if (!(INIT && base == 1)) {
+        if (!((INIT || !WS) && base == 1)) {
           const unsigned char* src = base == 0   ? reinterpret_cast<const unsigned char*>(a.V)
                                      : base == 1 ? reinterpret_cast<const unsigned char*>(a.W)
                                      : base == 2 ? reinterpret_cast<const unsigned char*>(a.val)
@@ -505,6 +507,11 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
       for (int gq = g0; gq < G; gq += NCWG) {
         const int kr = gq * RW + q;
         const int64_t p = c * kC + kr;
+        double2 wreg[CPL];
+        if (!WS && !INIT && p < a.n_loc) {  // old W straight from HBM, lands under the gathers
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) wreg[cc] = ld_stream(a.W + p * R + cc * LPR + t, pol);
+        }
         double2 u[CPL];
 #pragma unroll
         for (int cc = 0; cc < CPL; ++cc) u[cc] = make_double2(0.0, 0.0);
@@ -548,7 +555,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
             if (INIT) {
               w = make_double2(a.scale * uu.x, a.scale * uu.y);
             } else {
-              const double2 wo = sW[kr * R + col];
+              const double2 wo = WS ? sW[kr * R + col] : wreg[cc];
               w = make_double2(fma(a.scale, uu.x, -wo.x), fma(a.scale, uu.y, -wo.y));
             }
             st_stream(a.W + p * R + col, w, pol);
@@ -592,7 +599,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
 
 enum Feed { kDirect = 0, kStaged = 1, kTiled = 2 };
 
-template <int R, int LPR, int U, int FEED, int CS = 1>
+template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true>
 struct Variant {
   static cudaError_t launch(bool init, const SweepArgs& a, int grid, cudaStream_t s) {
     if constexpr (FEED == kStaged) {
@@ -602,12 +609,12 @@ struct Variant {
         aug_spmmv_staged<R, LPR, U, false><<<grid, kThreads, kStagedSmem, s>>>(a);
     } else if constexpr (FEED == kTiled) {
       const int smem = a.tl.stages * a.tl.stage_bytes;
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (init)
-        aug_spmmv_tiled<R, LPR, U, CS, true><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
+        aug_spmmv_tiled<R, LPR, U, CS, WS, true><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
       else
-        aug_spmmv_tiled<R, LPR, U, CS, false><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
+        aug_spmmv_tiled<R, LPR, U, CS, WS, false><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
     } else {
       if (init)
         aug_spmmv_direct<R, LPR, U, true><<<grid, kThreads, 0, s>>>(a);
@@ -621,8 +628,8 @@ struct Variant {
     if constexpr (FEED == kStaged) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_staged<R, LPR, U, false>, kThreads, kStagedSmem);
     } else if constexpr (FEED == kTiled) {
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_tiled<R, LPR, U, CS, false>, tiled_threads<LPR, CS>(),
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_tiled<R, LPR, U, CS, WS, false>, tiled_threads<LPR, CS>(),
                                                     dyn_smem);
     } else {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_direct<R, LPR, U, false>, kThreads, 0);
@@ -637,12 +644,15 @@ struct Entry {
   int R;
   const char* name;
   int feed;
+  bool wstage;
   LaunchFn launch;
   OccFn occ;
 };
-#define KPM_VARIANT(R, LPR, U, F, NAME) {R, NAME, F, Variant<R, LPR, U, F>::launch, Variant<R, LPR, U, F>::occupancy}
+#define KPM_VARIANT(R, LPR, U, F, NAME) {R, NAME, F, true, Variant<R, LPR, U, F>::launch, Variant<R, LPR, U, F>::occupancy}
 #define KPM_VARIANT_CS(R, LPR, U, CS, NAME) \
-  {R, NAME, kTiled, Variant<R, LPR, U, kTiled, CS>::launch, Variant<R, LPR, U, kTiled, CS>::occupancy}
+  {R, NAME, kTiled, true, Variant<R, LPR, U, kTiled, CS>::launch, Variant<R, LPR, U, kTiled, CS>::occupancy}
+#define KPM_VARIANT_WR(R, LPR, U, NAME) \
+  {R, NAME, kTiled, false, Variant<R, LPR, U, kTiled, 1, false>::launch, Variant<R, LPR, U, kTiled, 1, false>::occupancy}
 // First entry of each width is the default (chosen from the B200 measurements in DESIGN.md).
 const Entry kTable[] = {
     KPM_VARIANT(1, 1, 4, kTiled, "tiled.lpr1.u4"),
@@ -658,11 +668,13 @@ const Entry kTable[] = {
     KPM_VARIANT(8, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kDirect, "direct.lpr8.u4"),
     KPM_VARIANT(16, 8, 4, kTiled, "tiled.lpr8.u4"),
+    KPM_VARIANT_WR(16, 8, 4, "tiled.lpr8.u4.wr"),
     KPM_VARIANT_CS(16, 8, 4, 2, "tiled.lpr8.u4.cs2"),
     KPM_VARIANT(16, 16, 4, kTiled, "tiled.lpr16.u4"),
     KPM_VARIANT(16, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(16, 8, 4, kDirect, "direct.lpr8.u4"),
     KPM_VARIANT(32, 8, 4, kTiled, "tiled.lpr8.u4"),
+    KPM_VARIANT_WR(32, 8, 4, "tiled.lpr8.u4.wr"),
     KPM_VARIANT_CS(32, 8, 4, 2, "tiled.lpr8.u4.cs2"),
     KPM_VARIANT(32, 8, 2, kTiled, "tiled.lpr8.u2"),
     KPM_VARIANT(32, 16, 4, kStaged, "staged.lpr16.u4"),
@@ -699,18 +711,23 @@ bool variant_tiled(int R, int variant) {
   return e && e->feed == kTiled;
 }
 
+bool variant_wstage(int R, int variant) {
+  const Entry* e = find(R, variant);
+  return e && e->wstage;
+}
+
 static int round128(int64_t b) { return (int)((b + 127) / 128 * 128); }
 
-TileLayout plan_tiles(int R, int64_t max_other, int64_t max_width, int stages) {
+TileLayout plan_tiles(int R, int64_t max_other, int64_t max_width, int stages, bool with_w) {
   TileLayout tl;
   const int64_t v = round128((kC + max_other) * R * 16);
-  const int64_t w = round128(kC * R * 16);
+  const int64_t w = with_w ? round128(kC * R * 16) : 0;
   const int64_t val = round128(kC * max_width * 16);
   const int64_t lc = round128(kC * max_width * 2);
   const int64_t stage = v + w + val + lc;
-  // Two stages by default: more CTAs per SM (more producer streams and consumer warps)
-  // beat a deeper ring (B200 measurements).  `stages` may lower it.
-  int n = (int)std::min<int64_t>(stages > 0 ? stages : 2, kTileBudget / std::max<int64_t>(stage, 1));
+  // Three stages by default, fewer if they do not fit (R = 32: two): measured on B200 against
+  // 1, 2 and 4 stages; `stages` (env KPM_TILE_STAGES) overrides.
+  int n = (int)std::min<int64_t>(stages > 0 ? stages : 3, kTileBudget / std::max<int64_t>(stage, 1));
   if (n < 1) return tl;
   tl.stages = n;
   tl.stage_bytes = (int)stage;

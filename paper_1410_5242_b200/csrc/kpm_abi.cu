@@ -221,7 +221,7 @@ static void free_sell(DevSell& s) {
   cudaFree(s.cptr);
   cudaFree(s.perm);
   cudaFree(s.lcol);
-  for (int i = 0; i < 6; ++i) cudaFree(s.rec[i]);
+  for (int i = 0; i < 12; ++i) cudaFree(s.rec[i]);
   s = DevSell();
 }
 
@@ -469,22 +469,30 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   if ((st = ensure(ctx, (void**)&ctx->X1, &xcap, (size_t)n_rows_total * Rk, sizeof(double2))) != KPM_OK) return st;
   ctx->x_cap = xcap;
 
-  TileLayout plan = s.tiles_ok ? plan_tiles(Rk, s.max_other, s.max_width, std::min(ctx->tile_stages, 4)) : TileLayout();
   const int lg = __builtin_ctz(Rk);
-  if (plan.stages >= 1 && !ctx->sell.rec[lg] && !ctx->sell.rec_failed[lg]) {
-    std::vector<uint32_t> rec;
-    if (!build_tile_records(ctx->cptr_h, ctx->tiles, Rk, plan.off_w, plan.off_val, plan.off_lcol, rec)) {
-      ctx->sell.rec_failed[lg] = true;
-    } else {
-      size_t cap = 0;
-      st = ensure(ctx, (void**)&ctx->sell.rec[lg], &cap, rec.size() / 4, sizeof(uint4));
-      if (st != KPM_OK) return st;
-      KPM_CUDA(cudaMemcpy(ctx->sell.rec[lg], rec.data(), sizeof(uint32_t) * rec.size(), cudaMemcpyHostToDevice));
+  // tiled-feed plan (shared-memory layout + copy records) for one W placement
+  auto tiled_plan = [&](bool with_w, TileLayout& plan) -> kpm_status {
+    plan = s.tiles_ok ? plan_tiles(Rk, s.max_other, s.max_width, std::min(ctx->tile_stages, 4), with_w) : TileLayout();
+    const int ri = 2 * lg + (with_w ? 1 : 0);
+    if (plan.stages >= 1 && !ctx->sell.rec[ri] && !ctx->sell.rec_failed[ri]) {
+      std::vector<uint32_t> rec;
+      if (!build_tile_records(ctx->cptr_h, ctx->tiles, Rk, plan.off_w, plan.off_val, plan.off_lcol, rec)) {
+        ctx->sell.rec_failed[ri] = true;
+      } else {
+        size_t cap = 0;
+        kpm_status st2 = ensure(ctx, (void**)&ctx->sell.rec[ri], &cap, rec.size() / 4, sizeof(uint4));
+        if (st2 != KPM_OK) return st2;
+        KPM_CUDA(cudaMemcpy(ctx->sell.rec[ri], rec.data(), sizeof(uint32_t) * rec.size(), cudaMemcpyHostToDevice));
+      }
     }
-  }
-  if (!ctx->sell.rec[lg]) plan = TileLayout();
+    if (!ctx->sell.rec[ri]) plan = TileLayout();
+    return KPM_OK;
+  };
   auto usable = [&](int v) {
-    if (variant_tiled(Rk, v)) return plan.stages >= 1;
+    if (variant_tiled(Rk, v)) {
+      TileLayout pl;
+      return tiled_plan(variant_wstage(Rk, v), pl) == KPM_OK && pl.stages >= 1;
+    }
     if (variant_staged(Rk, v)) return s.max_width <= staged_max_width();
     return true;
   };
@@ -493,6 +501,9 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   if (!usable(variant))
     for (variant = 0; variant < variant_count(Rk) - 1 && !usable(variant); ++variant) {
     }
+  TileLayout plan;
+  if (variant_tiled(Rk, variant) && (st = tiled_plan(variant_wstage(Rk, variant), plan)) != KPM_OK) return st;
+  const int rec_index = 2 * lg + (variant_wstage(Rk, variant) ? 1 : 0);
   ctx->last_variant = variant_name(Rk, variant);
   const TileLayout tl = plan;
   const int dyn_smem = variant_tiled(Rk, variant) ? tl.stages * tl.stage_bytes : 0;
@@ -541,7 +552,7 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   sa.chunk_list = nullptr;
   sa.chunk_begin = 0;
   sa.chunk_end = s.n_chunks;
-  sa.rec = s.rec[lg];
+  sa.rec = s.rec[rec_index];
   sa.lcol = s.lcol;
   sa.tl = tl;
   sa.b = ctx->b;

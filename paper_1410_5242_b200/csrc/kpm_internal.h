@@ -25,8 +25,8 @@ struct DevSell {
   bool tiles_ok = false;
   uint16_t* lcol = nullptr;    // n_slots: column as index into the chunk's shared-memory tile
   int64_t max_other = 0, max_runs = 0;
-  uint4* rec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // copy records per log2(R)
-  bool rec_failed[6] = {false, false, false, false, false, false};
+  uint4* rec[12] = {};        // copy records per (log2(R), W staged)
+  bool rec_failed[12] = {};
 };
 
 // Shared-memory layout of one stage of the tiled feed (bytes, 128-B aligned sections).
@@ -73,7 +73,8 @@ bool variant_staged(int R, int variant);
 int staged_max_width();  // widest chunk (entries per row) the staged feed accepts
 bool variant_tiled(int R, int variant);
 // Shared-memory plan of the tiled feed for block width R, or stages == 0 if it does not fit.
-TileLayout plan_tiles(int R, int64_t max_other, int64_t max_width, int stages);  // stages 0 = default
+TileLayout plan_tiles(int R, int64_t max_other, int64_t max_width, int stages, bool with_w);  // stages 0 = default
+bool variant_wstage(int R, int variant);  // tiled feed: old W staged in shared memory
 cudaError_t launch_aug_spmmv(int R, int variant, bool init, const SweepArgs& a, int grid, cudaStream_t s);
 // eta[m][r] (double2) for m in [0, n_sweeps) from partials[m][3R][width] (width = launches x grid)
 cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int width, double2* eta_even,
