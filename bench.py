@@ -105,6 +105,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
+def cache_roofline(wavefronts, sm_mhz, sweep_ms, t_hbm_ms):
+    """The paper's custom roofline P* = min(P*_MEM, P*_LLC) (Eq. (11) `eq:roofline_custom`)
+    for the B200: the shared-memory data pipe moves one 128-B wavefront per cycle per SM, so a
+    sweep needs at least W / (148 f_SM) seconds for the W wavefronts ncu counted per launch
+    (profiles/traffic.json), at the SM clock sampled during the timed region."""
+    if not wavefronts or not sm_mhz:
+        return None
+    t_smem = wavefronts / (148 * sm_mhz * 1e6) * 1e3
+    t_bound = max(t_smem, t_hbm_ms)
+    return {"bound": "smem" if t_smem > t_hbm_ms else "hbm", "smem_wavefronts_per_launch": wavefronts,
+            "sm_mhz": sm_mhz, "t_smem_min_ms": t_smem, "t_hbm_min_ms": t_hbm_ms, "t_measured_ms": sweep_ms,
+            "frac_of_applicable": t_bound / sweep_ms,
+            "note": "wavefronts from ncu --set full (profiles/), peak 1 wavefront/clk/SM x 148 SMs"}
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -258,10 +273,12 @@ def main():
     bytes_sweep = alg_bytes_per_sweep(n_loc, nnz_loc, R)  # per rank per launch
     achieved = bytes_sweep / (sweep * 1e-3) / 1e9
     bmin = alg_bytes_per_sweep(n, nnz, R) / alg_flops_per_sweep(n, nnz, R)
-    traffic = None
+    traffic, smem_wf = None, None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
-        traffic = json.load(open(tf)).get(f"{px}x{ny}x{nz}/R{R}")
+        tj = json.load(open(tf))
+        traffic = tj.get(f"{px}x{ny}x{nz}/R{R}")
+        smem_wf = tj.get(f"{px}x{ny}x{nz}/R{R}/smem_wavefronts")
     out = {
         "metric": "augmented SpMMV Gflop/s (cplx dbl)", "value": value, "unit": "Gflop/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
@@ -278,6 +295,7 @@ def main():
                      "B_min_bytes_per_flop": bmin, "P_mem_gflops_per_gpu": hbm / bmin,
                      "kernel_gflops_per_gpu": alg_flops_per_sweep(n_loc, nnz_loc, R) / (sweep * 1e-3) / 1e9},
         "gpu_launches": args.steps * n_blocks * ((M // 2) * (2 if world > 1 else 1) + 2),
+        "cache_roofline": cache_roofline(smem_wf, clocks.get("sm_mhz"), sweep, bytes_sweep / hbm / 1e9 * 1e3),
         "clocks": clocks,
     }
     # R sweep of the same lattice (HBM -> cache bottleneck shift), shorter M

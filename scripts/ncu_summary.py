@@ -88,6 +88,8 @@ def main():
         lattice, r = tag.split("/")
         traffic[f"{lattice}/{r}"] = dram
         vals["dram_bytes_per_launch"] = dram
+        smem = float(d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"][1].replace(",", ""))
+        traffic[f"{lattice}/{r}/smem_wavefronts"] = smem
     if args.full:
         json.dump(traffic, open(traffic_path, "w"), indent=1, sort_keys=True)
         with open(os.path.join(prof, f"{args.round}_ncu_full.json"), "w") as f:
