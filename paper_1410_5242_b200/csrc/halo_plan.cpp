@@ -36,7 +36,7 @@ bool plan_send_runs(int peer, const std::vector<int64_t>& req, int64_t row_begin
   return true;
 }
 
-void plan_edge_chunks(const std::vector<int64_t>& cptr, const std::vector<int32_t>& col, int64_t n_pad, int C,
+void plan_edge_chunks(const std::vector<int64_t>& cptr, const int32_t* col, int64_t n_pad, int C,
                       const std::vector<SendRun>& sends, std::vector<int64_t>& edge, std::vector<int64_t>& interior) {
   const int64_t n_chunks = (int64_t)cptr.size() - 1;
   std::vector<char> is_edge(n_chunks, 0);

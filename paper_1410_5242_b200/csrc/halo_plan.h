@@ -35,7 +35,7 @@ bool plan_send_runs(int peer, const std::vector<int64_t>& req, int64_t row_begin
 
 // Chunks that must be computed before the exchange (they hold rows that are sent) or that
 // read halo slots; the rest are interior.  Both lists ascending.
-void plan_edge_chunks(const std::vector<int64_t>& cptr, const std::vector<int32_t>& col, int64_t n_pad, int C,
+void plan_edge_chunks(const std::vector<int64_t>& cptr, const int32_t* col, int64_t n_pad, int C,
                       const std::vector<SendRun>& sends, std::vector<int64_t>& edge, std::vector<int64_t>& interior);
 
 }  // namespace kpm

@@ -277,7 +277,7 @@ static kpm_status plan_exchange(kpm_ctx* ctx, const HostSell& hs) {
       return fail(ctx, KPM_EINVAL, "halo request does not map to contiguous local rows");
   }
   std::vector<int64_t> edge, interior;
-  plan_edge_chunks(hs.cptr, hs.col, hs.n_pad, hs.C, ctx->send_runs, edge, interior);
+  plan_edge_chunks(hs.cptr, hs.col.data(), hs.n_pad, hs.C, ctx->send_runs, edge, interior);
   ctx->n_edge = (int64_t)edge.size();
   ctx->n_interior = (int64_t)interior.size();
   KPM_CUDA(cudaMalloc(&ctx->edge_list, sizeof(int64_t) * std::max<size_t>(1, edge.size())));
@@ -409,7 +409,7 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
                             cudaMemcpyHostToDevice));
       }
     }
-    std::vector<uint16_t>().swap(ctx->tiles.lcol);  // host copy no longer needed
+    raw_vector<uint16_t>().swap(ctx->tiles.lcol);  // host copy no longer needed
   }
   ctx->halo = hs.halo;
   ctx->row_begins = row_begins;

@@ -9,8 +9,30 @@
 #include <algorithm>
 #include <numeric>
 #include <stdexcept>
+#include <thread>
 
 namespace kpm {
+
+// Static block partition of [0, n) over the host's cores (the build is one-off setup work,
+// but it sits inside the e2e path, so it uses every core).  f(begin, end, thread index).
+template <class F>
+static void parallel_for(int64_t n, F f) {
+  int T = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 64u);
+  if (n < 4096) T = 1;
+  std::vector<std::thread> th;
+  for (int t = 0; t < T; ++t) {
+    const int64_t b = n * t / T, e = n * (t + 1) / T;
+    if (t == T - 1)
+      f(b, e, t);
+    else
+      th.emplace_back(f, b, e, t);
+  }
+  for (auto& x : th) x.join();
+}
+
+static int n_threads_for(int64_t n) {
+  return n < 4096 ? 1 : (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 64u);
+}
 
 int build_sell_host(const int64_t* row_ptr, const int64_t* col, const double* val, int64_t n_loc,
                     int64_t row_begin, int64_t row_end, int C, int sigma, HostSell& out, std::string& err) {
@@ -39,10 +61,19 @@ int build_sell_host(const int64_t* row_ptr, const int64_t* col, const double* va
 
   // halo: distinct remote columns, ascending global id (== by owner rank, then id)
   std::vector<int64_t>& halo = out.halo;
-  for (int64_t k = 0; k < row_ptr[n_loc]; ++k)
-    if (col[k] < row_begin || col[k] >= row_end) halo.push_back(col[k]);
-  std::sort(halo.begin(), halo.end());
-  halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+  {
+    const int64_t nnz = row_ptr[n_loc];
+    std::vector<std::vector<int64_t>> part(n_threads_for(nnz));
+    parallel_for(nnz, [&](int64_t b, int64_t e, int t) {
+      for (int64_t k = b; k < e; ++k)
+        if (col[k] < row_begin || col[k] >= row_end) part[t].push_back(col[k]);
+      std::sort(part[t].begin(), part[t].end());
+      part[t].erase(std::unique(part[t].begin(), part[t].end()), part[t].end());
+    });
+    for (auto& v : part) halo.insert(halo.end(), v.begin(), v.end());
+    std::sort(halo.begin(), halo.end());
+    halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+  }
   out.n_halo = (int64_t)halo.size();
   if (out.n_pad + out.n_halo > (int64_t)INT32_MAX) {
     err = "local rows + halo rows exceed the int32 kernel index range";
@@ -59,9 +90,10 @@ int build_sell_host(const int64_t* row_ptr, const int64_t* col, const double* va
     out.cptr[c + 1] = out.cptr[c] + C * m;
   }
   const int64_t n_slots = out.cptr[out.n_chunks];
-  out.val.assign(2 * n_slots, 0.0);
+  out.val.resize(2 * n_slots);
   out.col.resize(n_slots);
-  for (int64_t c = 0; c < out.n_chunks; ++c) {
+  parallel_for(out.n_chunks, [&](int64_t cb, int64_t ce, int) {
+  for (int64_t c = cb; c < ce; ++c) {
     const int64_t L = (out.cptr[c + 1] - out.cptr[c]) / C;
     for (int64_t k = 0; k < C; ++k) {
       const int64_t p = c * C + k;
@@ -82,10 +114,13 @@ int build_sell_host(const int64_t* row_ptr, const int64_t* col, const double* va
           out.val[2 * d + 1] = val[2 * (src + j) + 1];
         } else {
           out.col[d] = (int32_t)p;  // padding: value 0, column = own position
+          out.val[2 * d] = 0.0;
+          out.val[2 * d + 1] = 0.0;
         }
       }
     }
   }
+  });
   return 0;
 }
 
@@ -96,8 +131,15 @@ void build_tiles_host(const HostSell& s, HostTiles& out) {
   out.run_ptr.assign(s.n_chunks + 1, 0);
   out.lcol.resize(n_slots);
   out.ok = true;
+  // pass 1 (parallel over chunks): lcol, per-chunk runs; pass 2: concatenate the runs
+  const int T = n_threads_for(s.n_chunks);
+  std::vector<std::vector<int32_t>> runs_t(T);
+  std::vector<int64_t> max_other_t(T, 0), max_runs_t(T, 0);
+  std::vector<char> ok_t(T, 1);
+  parallel_for(s.n_chunks, [&](int64_t cb, int64_t ce, int tt) {
   std::vector<int32_t> other;
-  for (int64_t c = 0; c < s.n_chunks; ++c) {
+  std::vector<int32_t>& runs = runs_t[tt];
+  for (int64_t c = cb; c < ce; ++c) {
     const int64_t a = s.cptr[c], b = s.cptr[c + 1];
     const int64_t own0 = c * C, own1 = own0 + C;
     other.clear();
@@ -105,20 +147,20 @@ void build_tiles_host(const HostSell& s, HostTiles& out) {
       if (s.col[k] < own0 || s.col[k] >= own1) other.push_back(s.col[k]);
     std::sort(other.begin(), other.end());
     other.erase(std::unique(other.begin(), other.end()), other.end());
-    if ((int64_t)other.size() + C > 65535) out.ok = false;
-    out.max_other = std::max<int64_t>(out.max_other, (int64_t)other.size());
+    if ((int64_t)other.size() + C > 65535) ok_t[tt] = 0;
+    max_other_t[tt] = std::max<int64_t>(max_other_t[tt], (int64_t)other.size());
     int64_t nr = 0;
     for (size_t i = 0; i < other.size(); ++i) {
       if (i == 0 || other[i] != other[i - 1] + 1) {
-        out.runs.push_back(other[i]);
-        out.runs.push_back(1);
+        runs.push_back(other[i]);
+        runs.push_back(1);
         ++nr;
       } else {
-        ++out.runs.back();
+        ++runs.back();
       }
     }
-    out.max_runs = std::max(out.max_runs, nr);
-    out.run_ptr[c + 1] = out.run_ptr[c] + nr;
+    max_runs_t[tt] = std::max(max_runs_t[tt], nr);
+    out.run_ptr[c + 1] = nr;  // count for now, prefix-summed below
     for (int64_t k = a; k < b; ++k) {
       const int32_t g = s.col[k];
       if (g >= own0 && g < own1) {
@@ -128,6 +170,14 @@ void build_tiles_host(const HostSell& s, HostTiles& out) {
         out.lcol[k] = (uint16_t)std::min<int64_t>(C + idx, 65535);
       }
     }
+  }
+  });
+  for (int64_t c = 0; c < s.n_chunks; ++c) out.run_ptr[c + 1] += out.run_ptr[c];
+  for (int t = 0; t < T; ++t) {
+    out.runs.insert(out.runs.end(), runs_t[t].begin(), runs_t[t].end());
+    out.ok = out.ok && ok_t[t];
+    out.max_other = std::max(out.max_other, max_other_t[t]);
+    out.max_runs = std::max(out.max_runs, max_runs_t[t]);
   }
 }
 

@@ -1,16 +1,41 @@
 #pragma once
 #include <stdint.h>
 
+#include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace kpm {
 
+// Allocator that leaves new elements uninitialised (the builders write every element), so
+// resizing the multi-GB SELL arrays does not zero-fill them first.
+template <class T>
+struct NoInit : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInit<U>;
+  };
+  NoInit() = default;
+  template <class U>
+  NoInit(const NoInit<U>&) {}
+  template <class U>
+  void construct(U* p) {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using raw_vector = std::vector<T, NoInit<T>>;
+
 struct HostSell {
   int64_t n_loc = 0, n_pad = 0, n_chunks = 0, n_halo = 0;
   int C = 32, sigma = 1;
-  std::vector<double> val;     // 2*n_slots (re, im)
-  std::vector<int32_t> col;    // n_slots
+  raw_vector<double> val;      // 2*n_slots (re, im)
+  raw_vector<int32_t> col;     // n_slots
   std::vector<int64_t> cptr;   // n_chunks+1
   std::vector<int32_t> perm;   // n_loc
   std::vector<int64_t> halo;   // n_halo global ids, ascending
@@ -24,7 +49,7 @@ struct HostTiles {
   bool ok = false;                 // false: some chunk needs > 65535 tile rows
   std::vector<int64_t> run_ptr;    // n_chunks+1, into runs
   std::vector<int32_t> runs;       // 2 per run: first row, row count
-  std::vector<uint16_t> lcol;      // n_slots
+  raw_vector<uint16_t> lcol;       // n_slots
   int64_t max_other = 0;           // max rows outside the own block, over chunks
   int64_t max_runs = 0;
 };
