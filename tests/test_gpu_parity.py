@@ -203,3 +203,24 @@ def test_dos_pipeline_c1(pkg):
     assert np.max(np.abs(rho - rho_o)) <= 1e-10 * np.max(rho_o)
     x = a * (E - b)
     assert np.pi / len(x) * np.sum(rho / a * np.sqrt(1 - x * x)) == pytest.approx(lat.n, rel=1e-12)
+
+
+@pytest.mark.parametrize("R", [1, 2, 4, 8, 16, 32])
+def test_every_kernel_variant(pkg, R, monkeypatch):
+    """Each aug_spmmv variant of a width (tiled / staged / direct feeds, lane maps, unrolls;
+    KPM_VARIANT) against the oracle, on a lattice with a ragged last chunk."""
+    lat, rp, col, val, a, b = problem((5, 6, 9))
+    M = 48
+    eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, SEED)
+    seen = set()
+    for v in range(12):
+        monkeypatch.setenv("KPM_VARIANT", str(v))
+        with pkg.KpmContext() as ctx:
+            ctx.set_matrix(rp, col, val, a, b)
+            mu, eta = ctx.moments(M, R, SEED)
+            name = ctx.last_kernel()
+        if name in seen:
+            break  # index past the last variant falls back to the default
+        seen.add(name)
+        check(eta, mu, eta_o)
+    assert len(seen) >= 2
