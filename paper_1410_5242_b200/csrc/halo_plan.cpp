@@ -31,7 +31,7 @@ bool plan_send_runs(int peer, const std::vector<int64_t>& req, int64_t row_begin
     const int64_t p0 = invperm[g0 - row_begin];
     for (int64_t k = 1; k < cnt; ++k)
       if (invperm[g0 + k - row_begin] != p0 + k) return false;
-    out.push_back(SendRun{peer, p0, cnt});
+    out.push_back(SendRun{peer, p0, cnt, -1});
   }
   return true;
 }

@@ -22,6 +22,7 @@ struct RecvRun {
 struct SendRun {
   int peer;
   int64_t pos, count;
+  int64_t peer_slot = -1;  // first halo slot of the run in the peer's vectors (fused exchange)
 };
 
 // Maximal runs of consecutive global ids in the (sorted) halo list, split at owner changes.

@@ -53,12 +53,14 @@ __global__ void z4_init_kernel(double2* __restrict__ V, double2* __restrict__ W,
       v = z4_phase(seed, (uint64_t)row, (uint32_t)(col_begin + r));
     }
     V[e] = v;
-    W[e] = make_double2(0.0, 0.0);
+    // W's halo slots are left alone: with the fused exchange the neighbours' init sweep may
+    // already be storing nu_1 into them.
+    if (p < n_pad) W[e] = make_double2(0.0, 0.0);
   }
 }
 
 __global__ void v0_permute_kernel(double2* __restrict__ V, double2* __restrict__ W, const double2* __restrict__ v0,
-                                  const int* __restrict__ perm, int64_t n_loc, int64_t n_total, int R,
+                                  const int* __restrict__ perm, int64_t n_loc, int64_t n_pad, int64_t n_total, int R,
                                   int r_valid) {
   const int64_t n_el = n_total * R;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x) {
@@ -70,7 +72,7 @@ __global__ void v0_permute_kernel(double2* __restrict__ V, double2* __restrict__
       v = v0[row * r_valid + r];
     }
     V[e] = v;
-    W[e] = make_double2(0.0, 0.0);
+    if (p < n_pad) W[e] = make_double2(0.0, 0.0);  // halo slots: see z4_init_kernel
   }
 }
 
@@ -105,6 +107,17 @@ __device__ __forceinline__ void st_stream(double2* ptr, double2 v, uint64_t pol)
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(ptr), "d"(v.x), "d"(v.y),
                "l"(pol)
                : "memory");
+}
+
+// Fused halo exchange: a boundary row's new value also goes straight into the neighbour's
+// halo slot (peer memory over NVLink); made visible by the stream-ordered system-scope
+// fence of the flag write that follows the launch (kpm_abi.cu).
+template <int R>
+__device__ __forceinline__ void store_peers(const SweepArgs& a, int64_t p, int col, double2 w) {
+  for (int i = 0; i < a.n_peer; ++i) {
+    const PeerRun& pr = a.peer[i];
+    if (p >= pr.pos && p < pr.pos + pr.count) pr.dst[(p - pr.pos) * R + col] = w;
+  }
 }
 
 // u += h * x  (complex multiply-add, 4 DFMA)
@@ -251,6 +264,7 @@ __device__ __forceinline__ void row_group(const SweepArgs& a, const double2* vp,
       else
         w = make_double2(fma(a.scale, uu.x, -wo[cc].x), fma(a.scale, uu.y, -wo[cc].y));
       st_stream(a.W + e, w, pol);
+      store_peers<R>(a, p, cc * LPR + t, w);
       d.ee[cc] = fma(vi.x, vi.x, fma(vi.y, vi.y, d.ee[cc]));
       // conj(w) * v = (wr vr + wi vi) + i (wr vi - wi vr)
       d.eor[cc] = fma(w.x, vi.x, fma(w.y, vi.y, d.eor[cc]));
@@ -559,6 +573,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
               w = make_double2(fma(a.scale, uu.x, -wo.x), fma(a.scale, uu.y, -wo.y));
             }
             st_stream(a.W + p * R + col, w, pol);
+            store_peers<R>(a, p, col, w);
             d.ee[cc] = fma(vi.x, vi.x, fma(vi.y, vi.y, d.ee[cc]));
             d.eor[cc] = fma(w.x, vi.x, fma(w.y, vi.y, d.eor[cc]));
             d.eoi[cc] = fma(w.x, vi.y, fma(-w.y, vi.x, d.eoi[cc]));
@@ -766,9 +781,9 @@ cudaError_t launch_z4_init(double2* V, double2* W, const int* perm, int64_t n_lo
 }
 
 cudaError_t launch_v0_upload_permute(double2* V, double2* W, const double2* v0_dev, const int* perm, int64_t n_loc,
-                                     int64_t n_rows_total, int R, int r_valid, cudaStream_t s) {
-  v0_permute_kernel<<<elementwise_grid(n_rows_total * R), 256, 0, s>>>(V, W, v0_dev, perm, n_loc, n_rows_total, R,
-                                                                        r_valid);
+                                     int64_t n_pad, int64_t n_rows_total, int R, int r_valid, cudaStream_t s) {
+  v0_permute_kernel<<<elementwise_grid(n_rows_total * R), 256, 0, s>>>(V, W, v0_dev, perm, n_loc, n_pad, n_rows_total,
+                                                                        R, r_valid);
   return cudaGetLastError();
 }
 

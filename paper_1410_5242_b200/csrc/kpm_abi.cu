@@ -12,7 +12,11 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
 #include <nccl.h>
+
+#include <array>
+#include <map>
 
 #include "../../include/kpm.h"
 #include "halo_plan.h"
@@ -68,6 +72,16 @@ struct kpm_ctx {
   int64_t* interior_list = nullptr; // device: the other chunks
   int64_t n_edge = 0, n_interior = 0;
   int64_t* halo_rows = nullptr;     // device: global id of each halo slot
+  // fused halo exchange (peer stores from the sweep epilogue + stream flag ops)
+  bool fused = false;               // chosen per set_matrix (env KPM_HALO=nccl|fused)
+  bool fused_ready = false;         // IPC mappings valid for the current X0/X1
+  int32_t* flags = nullptr;         // device: flags[src] = last sweep epoch whose halo src wrote
+  uint32_t epoch = 0;
+  std::map<std::string, void*> ipc_open;  // opened peer handles (by handle bytes)
+  std::vector<std::array<double2*, 2>> dst_x;  // per send run: peer's X0/X1 + (peer n_pad + slot)*Rk
+  std::vector<int32_t*> dst_flag;   // per destination peer (parallel to dest_peers)
+  std::vector<int> dest_peers, src_peers;
+  int fused_rk = 0;
   double last_total_ms = 0.0, last_sweep_ms = 0.0;
   int last_n_sweeps = 0;
 };
@@ -93,6 +107,8 @@ static std::string g_create_err;
       return KPM_ECUDA;                                                             \
     }                                                                               \
   } while (0)
+
+static bool load_stream_memops();
 
 static kpm_status fail(kpm_ctx* ctx, kpm_status st, const std::string& msg) {
   ctx->err = msg;
@@ -181,6 +197,8 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   cudaFree(ctx->edge_list);
   cudaFree(ctx->interior_list);
   cudaFree(ctx->halo_rows);
+  for (auto& kv : ctx->ipc_open) cudaIpcCloseMemHandle(kv.second);
+  cudaFree(ctx->flags);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->ev_edge) cudaEventDestroy(ctx->ev_edge);
@@ -233,9 +251,10 @@ static kpm_status plan_exchange(kpm_ctx* ctx, const HostSell& hs) {
   ctx->recv_runs = plan_recv_runs(hs.halo, ctx->row_begins);
   // requests: per owner q the (gfirst, count) pairs, in slot order
   std::vector<std::vector<int64_t>> req(P);
-  for (const RecvRun& r : ctx->recv_runs) {
+  for (const RecvRun& r : ctx->recv_runs) {  // (first global row, count, first halo slot)
     req[r.peer].push_back(r.gfirst);
     req[r.peer].push_back(r.count);
+    req[r.peer].push_back(r.slot);
   }
   std::vector<int64_t> counts(P), all;
   for (int q = 0; q < P; ++q) counts[q] = (int64_t)req[q].size();
@@ -271,10 +290,17 @@ static kpm_status plan_exchange(kpm_ctx* ctx, const HostSell& hs) {
   int64_t off = 0;
   for (int p = 0; p < P; ++p) {
     const int64_t n = all[(size_t)p * P + me];
-    std::vector<int64_t> rq(incoming.begin() + off, incoming.begin() + off + n);
+    std::vector<int64_t> rq, slots;
+    for (int64_t i = off; i + 2 < off + n; i += 3) {
+      rq.push_back(incoming[i]);
+      rq.push_back(incoming[i + 1]);
+      slots.push_back(incoming[i + 2]);
+    }
     off += n;
+    const size_t first = ctx->send_runs.size();
     if (!plan_send_runs(p, rq, row_begin, row_end, hs.perm, ctx->send_runs))
       return fail(ctx, KPM_EINVAL, "halo request does not map to contiguous local rows");
+    for (size_t i = first; i < ctx->send_runs.size(); ++i) ctx->send_runs[i].peer_slot = slots[i - first];
   }
   std::vector<int64_t> edge, interior;
   plan_edge_chunks(hs.cptr, hs.col.data(), hs.n_pad, hs.C, ctx->send_runs, edge, interior);
@@ -421,9 +447,36 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
   ctx->edge_list = ctx->interior_list = ctx->halo_rows = nullptr;
   ctx->n_edge = 0;
   ctx->n_interior = d.n_chunks;
+  ctx->fused = false;
+  ctx->fused_ready = false;
   if (ctx->opt.nranks > 1) {
     kpm_status st1 = plan_exchange(ctx, hs);
     if (st1 != KPM_OK) return st1;
+    const char* mode = getenv("KPM_HALO");
+    ctx->fused = !(mode && std::string(mode) == "nccl") && ctx->send_runs.size() <= (size_t)kMaxPeerRuns &&
+                 load_stream_memops();
+    if (ctx->fused) {  // Hermitian => symmetric pattern => I receive from exactly the ranks I send to
+      std::vector<int> d, r;
+      for (const SendRun& x : ctx->send_runs) d.push_back(x.peer);
+      for (const RecvRun& x : ctx->recv_runs) r.push_back(x.peer);
+      std::sort(d.begin(), d.end());
+      d.erase(std::unique(d.begin(), d.end()), d.end());
+      std::sort(r.begin(), r.end());
+      r.erase(std::unique(r.begin(), r.end()), r.end());
+      ctx->dest_peers = d;
+      ctx->src_peers = r;
+      if (d != r) ctx->fused = false;
+    }
+    // the mode must agree on all ranks
+    std::vector<int64_t> all;
+    kpm_status st2 = allgather_i64(ctx, {ctx->fused ? 1 : 0}, all);
+    if (st2 != KPM_OK) return st2;
+    for (int64_t v : all) ctx->fused = ctx->fused && v == 1;
+    if (ctx->fused && !ctx->flags) {
+      KPM_CUDA(cudaMalloc(&ctx->flags, sizeof(int32_t) * ctx->opt.nranks));
+      KPM_CUDA(cudaMemset(ctx->flags, 0, sizeof(int32_t) * ctx->opt.nranks));
+      ctx->epoch = 0;
+    }
   }
   ctx->n_global = H->n_global;
   ctx->row_begin = H->row_begin;
@@ -454,6 +507,79 @@ static kpm_status ensure(kpm_ctx* ctx, void** p, size_t* cap, size_t need, size_
   return KPM_OK;
 }
 
+// Driver stream memory operations (wait / write a 32-bit flag), resolved at run time through
+// the runtime's entry-point query, so the library needs no link-time libcuda.
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WaitValue32Fn g_wait_value32 = nullptr;
+static WriteValue32Fn g_write_value32 = nullptr;
+
+static bool load_stream_memops() {
+  if (g_wait_value32 && g_write_value32) return true;
+  cudaDriverEntryPointQueryResult q1, q2;
+  void *f1 = nullptr, *f2 = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f1, cudaEnableDefault, &q1) != cudaSuccess ||
+      q1 != cudaDriverEntryPointSuccess)
+    return false;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f2, cudaEnableDefault, &q2) != cudaSuccess ||
+      q2 != cudaDriverEntryPointSuccess)
+    return false;
+  g_wait_value32 = reinterpret_cast<WaitValue32Fn>(f1);
+  g_write_value32 = reinterpret_cast<WriteValue32Fn>(f2);
+  return true;
+}
+
+// Fused exchange setup (collective): every rank publishes CUDA IPC handles of X0, X1 and
+// its flag array plus its n_pad; each rank maps the buffers of the peers it sends to and
+// precomputes, per send run, the destination address of the run in the peer's halo slots.
+static kpm_status setup_fused(kpm_ctx* ctx, int Rk) {
+  struct Pub {
+    cudaIpcMemHandle_t x0, x1, fl;
+    int64_t n_pad;
+  };
+  static_assert(sizeof(Pub) % 8 == 0, "Pub must be int64-aligned");
+  Pub mine;
+  KPM_CUDA(cudaIpcGetMemHandle(&mine.x0, ctx->X0));
+  KPM_CUDA(cudaIpcGetMemHandle(&mine.x1, ctx->X1));
+  KPM_CUDA(cudaIpcGetMemHandle(&mine.fl, ctx->flags));
+  mine.n_pad = ctx->sell.n_pad;
+  std::vector<int64_t> v(sizeof(Pub) / 8), all;
+  std::memcpy(v.data(), &mine, sizeof(Pub));
+  kpm_status st = allgather_i64(ctx, v, all);
+  if (st != KPM_OK) return st;
+  const int P = ctx->opt.nranks;
+  std::vector<Pub> pubs(P);
+  for (int q = 0; q < P; ++q) std::memcpy(&pubs[q], all.data() + (size_t)q * v.size(), sizeof(Pub));
+  auto open = [&](const cudaIpcMemHandle_t& h, void** out) -> kpm_status {
+    const std::string key(reinterpret_cast<const char*>(&h), sizeof(h));
+    auto it = ctx->ipc_open.find(key);
+    if (it == ctx->ipc_open.end()) {
+      void* p = nullptr;
+      KPM_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      it = ctx->ipc_open.emplace(key, p).first;
+    }
+    *out = it->second;
+    return KPM_OK;
+  };
+  ctx->dst_x.clear();
+  for (const SendRun& r : ctx->send_runs) {
+    void *x0, *x1;
+    if ((st = open(pubs[r.peer].x0, &x0)) != KPM_OK) return st;
+    if ((st = open(pubs[r.peer].x1, &x1)) != KPM_OK) return st;
+    const int64_t off = (pubs[r.peer].n_pad + r.peer_slot) * Rk;
+    ctx->dst_x.push_back({static_cast<double2*>(x0) + off, static_cast<double2*>(x1) + off});
+  }
+  ctx->dst_flag.clear();
+  for (int q : ctx->dest_peers) {
+    void* fl;
+    if ((st = open(pubs[q].fl, &fl)) != KPM_OK) return st;
+    ctx->dst_flag.push_back(static_cast<int32_t*>(fl) + ctx->opt.rank);
+  }
+  ctx->fused_ready = true;
+  ctx->fused_rk = Rk;
+  return KPM_OK;
+}
+
 // One block of up to 32 columns: start block, M/2 sweeps, eta reduction, D2H.
 // eta_cols: host, [(r*M + n)] double2 for the rb columns of this block.
 static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint64_t seed, const double* v0,
@@ -467,7 +593,15 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   if ((st = ensure(ctx, (void**)&ctx->X0, &xcap, (size_t)n_rows_total * Rk, sizeof(double2))) != KPM_OK) return st;
   xcap = ctx->x_cap;
   if ((st = ensure(ctx, (void**)&ctx->X1, &xcap, (size_t)n_rows_total * Rk, sizeof(double2))) != KPM_OK) return st;
+  if (xcap != ctx->x_cap) ctx->fused_ready = false;
   ctx->x_cap = xcap;
+  if (ctx->opt.nranks > 1 && ctx->fused) {  // collective: re-publish when any rank's buffers changed
+    std::vector<int64_t> all;
+    if ((st = allgather_i64(ctx, {ctx->fused_ready && ctx->fused_rk == Rk ? 1 : 0}, all)) != KPM_OK) return st;
+    bool ready = true;
+    for (int64_t v : all) ready = ready && v == 1;
+    if (!ready && (st = setup_fused(ctx, Rk)) != KPM_OK) return st;
+  }
 
   const int lg = __builtin_ctz(Rk);
   // tiled-feed plan (shared-memory layout + copy records) for one W placement
@@ -538,7 +672,7 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     if ((st = ensure(ctx, (void**)&ctx->v0_dev, &vcap, (size_t)s.n_loc * rb, sizeof(double2))) != KPM_OK) return st;
     ctx->v0_cap = vcap;
     KPM_CUDA(cudaMemcpyAsync(ctx->v0_dev, v0, sizeof(double2) * s.n_loc * rb, cudaMemcpyHostToDevice, str));
-    KPM_CUDA(launch_v0_upload_permute(ctx->X0, ctx->X1, ctx->v0_dev, s.perm, s.n_loc, n_rows_total, Rk, rb, str));
+    KPM_CUDA(launch_v0_upload_permute(ctx->X0, ctx->X1, ctx->v0_dev, s.perm, s.n_loc, s.n_pad, n_rows_total, Rk, rb, str));
     if (multi && (st = exchange_halo(ctx, ctx->X0, Rk, str)) != KPM_OK) return st;
   } else {  // halo slots get their Z4 values directly from their global ids: no exchange for nu_0
     KPM_CUDA(launch_z4_init(ctx->X0, ctx->X1, s.perm, s.n_loc, s.n_pad, ctx->halo_rows, n_rows_total, Rk,
@@ -557,6 +691,7 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   sa.tl = tl;
   sa.b = ctx->b;
   sa.pstride = (int64_t)grid * parts;
+  sa.n_peer = 0;
   // One sweep m (m = 0: init sweep W = a(H - b)V; m >= 1: W <- 2a(H - b)V - W), with the
   // fused eta_2m, eta_2m+1 partials.  Multi-rank: edge chunks first, then the new boundary
   // rows go to the neighbours on the comm stream while the interior chunks run (a5).
@@ -571,11 +706,36 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
       KPM_CUDA(launch_aug_spmmv(Rk, variant, init, sa, grid, str));
       return KPM_OK;
     }
-    if (m > 0) KPM_CUDA(cudaStreamWaitEvent(str, ctx->ev_halo, 0));  // V's halo slots have arrived
     sa.chunk_list = ctx->edge_list;
     sa.chunk_begin = 0;
     sa.chunk_end = ctx->n_edge;
     sa.partials = part;
+    if (ctx->fused) {
+      // V's halo slots were written by the neighbours' previous edge launch: wait for their flags
+      if (m > 0)
+        for (int q : ctx->src_peers)
+          if (g_wait_value32(str, (CUdeviceptr)(ctx->flags + q), ctx->epoch, CU_STREAM_WAIT_VALUE_GEQ) !=
+              CUDA_SUCCESS)
+            return fail(ctx, KPM_ECUDA, "cuStreamWaitValue32 failed");
+      const bool send = m + 1 < n_sweeps;
+      sa.n_peer = send ? (int)ctx->send_runs.size() : 0;
+      for (int i = 0; i < sa.n_peer; ++i)
+        sa.peer[i] = PeerRun{ctx->send_runs[i].pos, ctx->send_runs[i].count, ctx->dst_x[i][(m + 1) & 1]};
+      KPM_CUDA(launch_aug_spmmv(Rk, variant, init, sa, grid, str));
+      sa.n_peer = 0;
+      if (send) {
+        ++ctx->epoch;
+        for (int32_t* f : ctx->dst_flag)
+          if (g_write_value32(str, (CUdeviceptr)f, ctx->epoch, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+            return fail(ctx, KPM_ECUDA, "cuStreamWriteValue32 failed");
+      }
+      sa.chunk_list = ctx->interior_list;
+      sa.chunk_end = ctx->n_interior;
+      sa.partials = part + grid;
+      KPM_CUDA(launch_aug_spmmv(Rk, variant, init, sa, grid, str));
+      return KPM_OK;
+    }
+    if (m > 0) KPM_CUDA(cudaStreamWaitEvent(str, ctx->ev_halo, 0));  // V's halo slots have arrived
     KPM_CUDA(launch_aug_spmmv(Rk, variant, init, sa, grid, str));
     if (m + 1 < n_sweeps) {
       KPM_CUDA(cudaEventRecord(ctx->ev_edge, str));

@@ -36,7 +36,15 @@ struct TileLayout {
   int off_w = 0, off_val = 0, off_lcol = 0;  // V tile rows start at 0
 };
 
-// One aug_spmmv sweep over the row groups [group_begin, group_end).
+// Fused halo exchange: rows [pos, pos+count) of the new W are also stored to dst (a peer
+// GPU's halo slots, mapped over NVLink with CUDA IPC) by the sweep kernel's epilogue.
+constexpr int kMaxPeerRuns = 8;
+struct PeerRun {
+  int64_t pos, count;
+  double2* dst;
+};
+
+// One aug_spmmv sweep over a chunk range / chunk list.
 struct SweepArgs {
   const double2* val;
   const int* col;
@@ -54,6 +62,9 @@ struct SweepArgs {
   const uint4* rec;      // kRecSlots per chunk (sell_build.h)
   const uint16_t* lcol;
   TileLayout tl;
+  // fused halo exchange (edge launches only; n_peer = 0 otherwise)
+  int n_peer;
+  PeerRun peer[kMaxPeerRuns];
 };
 
 // Launch helpers (kernels.cu).  All return cudaGetLastError() of the launch.
@@ -63,7 +74,7 @@ cudaError_t launch_z4_init(double2* V, double2* W, const int* perm, int64_t n_lo
                            int64_t n_rows_total, int R, int64_t row_begin, int64_t col_begin, int r_valid,
                            uint64_t seed, cudaStream_t s);
 cudaError_t launch_v0_upload_permute(double2* V, double2* W, const double2* v0_dev, const int* perm,
-                                     int64_t n_loc, int64_t n_rows_total, int R, int r_valid,
+                                     int64_t n_loc, int64_t n_pad, int64_t n_rows_total, int R, int r_valid,
                                      cudaStream_t s);
 // Kernel variants per block width R (feed x lanes-per-row x unroll); variant 0 is the default.
 int variant_count(int R);
