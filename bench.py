@@ -31,7 +31,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from workloads.ti_lattice import SEED, Lattice, gershgorin, generate_csr, scale_factors  # noqa: E402
+from workloads.ti_lattice import (CONFIGS, SEED, Lattice, chunk_order_yband, gershgorin, generate_csr,  # noqa: E402
+                                  scale_factors)
 
 S_D, S_I = 16, 4
 
@@ -153,7 +154,7 @@ def oracle_sample(rp, col, val, a, b, n, nnz, target_s=15.0, max_sweeps=400):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    nx, ny, nz = 200, 100, 40
+    nx, ny, nz = (200, 100, 40) if args.config == "bar" else CONFIGS[args.config]["lattice"]
     lat, rp, col, val, a, b = build_problem(nx, ny, nz)
     nnz = int(rp[-1])
     threads = host_cores()
@@ -167,12 +168,13 @@ def run_reference(args, rank, world):
         oracle.kpm_eta(rp, col, val, a, b, 2 * sweeps, 1, SEED, threads=threads)
     t = time.perf_counter() - t0
     value = args.steps * sweeps * alg_flops_per_sweep(lat.n, nnz, 1) / t / 1e9
-    sample = f"C3 lattice {nx}x{ny}x{nz} (N={lat.n}, N_nz={nnz}), 1 random vector, {sweeps} sweeps per step"
+    sample = f"lattice {nx}x{ny}x{nz} (N={lat.n}, N_nz={nnz}), 1 random vector, {sweeps} sweeps per step"
     print(json.dumps({
         "impl": "reference", "metric": "augmented SpMMV Gflop/s (cplx dbl)", "value": value, "unit": "Gflop/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": "C3 (oracle sample)", "lattice": [nx, ny, nz], "M": 2 * sweeps, "R": 1},
+        "config": {"workload": f"{'C3' if args.config == 'bar' else args.config} (oracle sample)",
+                   "lattice": [nx, ny, nz], "M": 2 * sweeps, "R": 1},
         "cpu_baseline": {"value": value, "unit": "Gflop/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "Gflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -184,9 +186,14 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--M", type=int, default=2000)
-    ap.add_argument("--R", type=int, default=32)
-    ap.add_argument("--lattice", default="200,100,40", help="per-GPU x-slab nx,ny,nz")
+    ap.add_argument("--M", type=int, default=None, help="default: the config's M (2000 for bar)")
+    ap.add_argument("--R", type=int, default=None, help="default: the config's R (32 for bar)")
+    ap.add_argument("--lattice", default="200,100,40", help="per-GPU x-slab nx,ny,nz (config bar)")
+    ap.add_argument("--config", default="bar", choices=["bar", "C1", "C2", "C3", "C4"],
+                    help="bar: (200N)x100x40 weak scaling (= C3 at N=1); C1..C4: the BASELINE.json lattices, "
+                         "global size fixed (strong scaling over N)")
+    ap.add_argument("--chunk-order", default="auto", choices=["auto", "none"],
+                    help="auto: y-banded chunk order when the x-neighbour window exceeds ~32 MB (kpm_set_chunk_order)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-r-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -221,9 +228,17 @@ def main():
         if dist is not None:
             dist.barrier()
 
-    # Bar weak scaling: x grows with the GPU count, each rank owns one C3-sized x-slab
-    px, ny, nz = (int(t) for t in args.lattice.split(","))
-    nx = px * world
+    if args.config == "bar":
+        # Bar weak scaling: x grows with the GPU count, each rank owns one C3-sized x-slab
+        px, ny, nz = (int(t) for t in args.lattice.split(","))
+        nx = px * world
+        scaling = "weak"
+    else:
+        nx, ny, nz = CONFIGS[args.config]["lattice"]
+        px = nx // world
+        if px * world != nx:
+            raise SystemExit(f"{args.config}: Nx={nx} not divisible by {world} ranks")
+        scaling = "strong"
     lat = Lattice(nx, ny, nz)
     x0, x1 = px * rank, px * (rank + 1)
     rp, col, val = generate_csr(lat, x0, x1)
@@ -232,7 +247,10 @@ def main():
     a, b = scale_factors(lo, hi)
     n, nnz = lat.n, lat.nnz_expected()
     n_loc, nnz_loc = len(rp) - 1, int(rp[-1])
-    M, R = args.M, args.R
+    if args.config == "bar":
+        M, R = args.M or 2000, args.R or 32
+    else:
+        M, R = args.M or CONFIGS[args.config]["M"], args.R or CONFIGS[args.config]["R"]
     uid = None
     if world > 1:
         box = [kpm.get_unique_id() if rank == 0 else None]
@@ -250,6 +268,15 @@ def main():
         os.close(saved)
     row_begin = x0 * lat.rows_per_plane
     ctx.set_matrix(rp, col, val, a, b, n_global=n, row_begin=row_begin)
+    band = None
+    if args.chunk_order == "auto" and 2 * lat.rows_per_plane * min(R, 32) * 16 > 32e6 and lat.nz % 8 == 0:
+        band = max(1, int(16e6 // (2 * 4 * nz * min(R, 32) * 16)))
+        order = chunk_order_yband(lat, x0, x1, band)
+
+        def apply_order():
+            ctx.set_chunk_order(order)
+
+        apply_order()
     n_blocks = (R + 31) // 32
 
     for _ in range(args.warmup):
@@ -282,12 +309,16 @@ def main():
     out = {
         "metric": "augmented SpMMV Gflop/s (cplx dbl)", "value": value, "unit": "Gflop/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": (f"C3 TI lattice {nx}x{ny}x{nz} x 4 orbitals, M={M}, R={R}" if world == 1 else
+        "scaling": scaling, "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": (f"{args.config} TI lattice {nx}x{ny}x{nz} x 4 orbitals, M={M}, R={R}"
+                                if args.config != "bar" else
+                                f"C3 TI lattice {nx}x{ny}x{nz} x 4 orbitals, M={M}, R={R}" if world == 1 else
                                 f"Bar TI lattice {nx}x{ny}x{nz} x 4 orbitals (C3 slab per GPU), M={M}, R={R}"),
                    "lattice": [nx, ny, nz], "N": n, "N_nz": nnz, "M": M, "R": R, "parallelism": f"x-slab dp{world}",
-                   "kernel_variant": ctx.last_kernel(),
-                   "l2": "inputs larger than L2 (V, W %.2f GB each per GPU; matrix %.2f GB)" % (
+                   "kernel_variant": ctx.last_kernel(), "chunk_order": f"y-band {band}" if band else "storage", "halo": os.environ.get("KPM_HALO", "fused") if world > 1 else None,
+                   "l2": ("inputs larger than L2 (V, W %.2f GB each per GPU; matrix %.2f GB)" if
+                          (32 * R * n_loc + 20 * nnz_loc) > 126e6 else
+                          "L2-resident working set (V, W %.2f GB each, matrix %.2f GB; no flush)") % (
                        16 * R * n_loc / 1e9, 20 * nnz_loc / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "kernel": "aug_spmmv main sweep (per GPU)", "sweep_ms": sweep,
@@ -319,6 +350,8 @@ def main():
         e0.record(stream)
         for _ in range(args.steps):
             ctx.set_matrix(rp, col, val, a, b, n_global=n, row_begin=row_begin)
+            if band:
+                apply_order()
             ctx.moments(M, R, SEED, want_eta=True)
         e1.record(stream)
         barrier()

@@ -93,6 +93,14 @@ kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt);
  * matrix. */
 kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, double b);
 
+/* Optional locality hint: the order in which the sweep kernels visit the n = n_chunks SELL
+ * chunks (a permutation of 0..n_chunks-1, host array; NULL restores storage order).  The
+ * moments are unchanged up to the rounding of the eta sums (which stay deterministic).  For
+ * stencil matrices whose neighbour window exceeds L2 (e.g. the 400x400x40 TI at R = 32,
+ * 65 MB), a banded order keeps the gathered rows L2-resident.
+ * Reset by kpm_set_matrix. */
+kpm_status kpm_set_chunk_order(kpm_ctx* ctx, const int64_t* order, int64_t n);
+
 /* KPM-DOS moments with R random start vectors |rand()>: Z4 phases
  * {1, i, -1, -i} from Philox4x32-10 keyed by (global row, global column, seed) (DESIGN.md
  * R6), so the result does not depend on nranks or the SELL permutation.

@@ -22,7 +22,7 @@ STATUS_NAMES = ["KPM_OK", "KPM_EINVAL", "KPM_ESTATE", "KPM_ERANGE", "KPM_ENOMEM"
 # exported symbols declared in include/kpm.h
 ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_dos", "kpm_export_sell", "kpm_get_sell_info", "kpm_get_unique_id",
                "kpm_last_error", "kpm_last_kernel", "kpm_last_timing", "kpm_moments", "kpm_moments_v0",
-               "kpm_plan_recv", "kpm_plan_send", "kpm_set_matrix"]
+               "kpm_plan_recv", "kpm_plan_send", "kpm_set_chunk_order", "kpm_set_matrix"]
 
 
 class KpmError(RuntimeError):
@@ -73,6 +73,7 @@ def load_library():
     lib.kpm_last_kernel.argtypes = [P]
     lib.kpm_last_kernel.restype = ctypes.c_char_p
     lib.kpm_get_unique_id.argtypes = [P]
+    lib.kpm_set_chunk_order.argtypes = [P, P, i64]
     lib.kpm_dos.argtypes = [i32, P, dbl, dbl, i32, P, i32, P, P]
     lib.kpm_plan_recv.argtypes = [i32, P, i32, P, P, P, P]
     lib.kpm_plan_send.argtypes = [i64, i64, i32, i64, P, P, P]
@@ -190,6 +191,14 @@ class KpmContext:
         csr = kpm_csr(n_global, row_begin, row_begin + n_loc, _ptr(row_ptr), _ptr(col), _ptr(val), mem)
         self._check(self.lib.kpm_set_matrix(self.h, ctypes.byref(csr), float(a), float(b)))
         del keep
+
+    def set_chunk_order(self, order=None):
+        """kpm_set_chunk_order: locality hint (permutation of the SELL chunks) or None."""
+        if order is None:
+            self._check(self.lib.kpm_set_chunk_order(self.h, None, 0))
+            return
+        o = np.ascontiguousarray(order, dtype=np.int64)
+        self._check(self.lib.kpm_set_chunk_order(self.h, _ptr(o), len(o)))
 
     def moments(self, M, R, seed, want_eta=True, allow_warning=True):
         """(mu (M,), eta (R, M) complex or None)."""

@@ -79,6 +79,13 @@ __global__ void v0_permute_kernel(double2* __restrict__ V, double2* __restrict__
 // ------------------------------------------------------------- memory helpers ------
 // Matrix entries and the old W are streamed once per sweep: bypass L1 and mark them
 // evict-first in L2 so that L1/L2 keep the gathered V rows.
+// Gathered V rows are reused across ~2 x-planes of the sweep (the x-neighbour window, 65 MB
+// at C4, R = 32): keep them in L2 ahead of the streamed matrix / W lines.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -468,6 +475,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
     // Lane i < 16 holds slot i of the chunk's copy record (header + up to 15 bulk copies);
     // the record of tile k+1 is loaded while tile k is issued, so no metadata load sits on
     // the producer's critical path.
+    const uint64_t pol_v = a.v_evict_last ? policy_evict_last() : 0ull;
     int64_t c_nxt = my_tiles > 0 ? chunk_at(a, blockIdx.x) : 0;
     uint4 nxt = my_tiles > 0 && lane < 16 ? __ldg(a.rec + c_nxt * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
     for (int64_t k = 0; k < my_tiles; ++k) {
@@ -499,7 +507,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
                                      : base == 1 ? reinterpret_cast<const unsigned char*>(a.W)
                                      : base == 2 ? reinterpret_cast<const unsigned char*>(a.val)
                                                  : reinterpret_cast<const unsigned char*>(a.lcol);
-          bulk_g2s(smem_u32(st + cur.z), src + off, bytes, bar, base == 0 ? 0ull : pol);
+          bulk_g2s(smem_u32(st + cur.z), src + off, bytes, bar, base == 0 ? pol_v : pol);
         }
       }
     }

@@ -71,6 +71,9 @@ struct kpm_ctx {
   int64_t* edge_list = nullptr;     // device: chunks holding sent rows or reading halo slots
   int64_t* interior_list = nullptr; // device: the other chunks
   int64_t n_edge = 0, n_interior = 0;
+  std::vector<char> edge_flag;      // host: chunk is an edge chunk
+  std::vector<int64_t> order_h;     // chunk processing order (kpm_set_chunk_order), empty = storage order
+  int64_t* order_list = nullptr;    // device copy for single-rank sweeps
   int64_t* halo_rows = nullptr;     // device: global id of each halo slot
   // fused halo exchange (peer stores from the sweep epilogue + stream flag ops)
   bool fused = false;               // chosen per set_matrix (env KPM_HALO=nccl|fused)
@@ -198,6 +201,7 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   cudaFree(ctx->interior_list);
   cudaFree(ctx->halo_rows);
   for (auto& kv : ctx->ipc_open) cudaIpcCloseMemHandle(kv.second);
+  cudaFree(ctx->order_list);
   cudaFree(ctx->flags);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
@@ -304,18 +308,62 @@ static kpm_status plan_exchange(kpm_ctx* ctx, const HostSell& hs) {
   }
   std::vector<int64_t> edge, interior;
   plan_edge_chunks(hs.cptr, hs.col.data(), hs.n_pad, hs.C, ctx->send_runs, edge, interior);
-  ctx->n_edge = (int64_t)edge.size();
-  ctx->n_interior = (int64_t)interior.size();
+  ctx->edge_flag.assign(hs.n_chunks, 0);
+  for (int64_t c : edge) ctx->edge_flag[c] = 1;
   KPM_CUDA(cudaMalloc(&ctx->edge_list, sizeof(int64_t) * std::max<size_t>(1, edge.size())));
   KPM_CUDA(cudaMalloc(&ctx->interior_list, sizeof(int64_t) * std::max<size_t>(1, interior.size())));
   KPM_CUDA(cudaMalloc(&ctx->halo_rows, sizeof(int64_t) * std::max<size_t>(1, hs.halo.size())));
+  if (!hs.halo.empty())
+    KPM_CUDA(cudaMemcpy(ctx->halo_rows, hs.halo.data(), sizeof(int64_t) * hs.halo.size(), cudaMemcpyHostToDevice));
+  return KPM_OK;
+}
+
+// Work lists of the sweep launches in the current chunk order: single rank -> order_list (or
+// the plain range when no order is set); multi-rank -> edge and interior lists, each in order.
+static kpm_status apply_order(kpm_ctx* ctx) {
+  const int64_t n = ctx->sell.n_chunks;
+  std::vector<int64_t> ord = ctx->order_h;
+  if (ord.empty()) {
+    ord.resize(n);
+    for (int64_t c = 0; c < n; ++c) ord[c] = c;
+  }
+  cudaFree(ctx->order_list);
+  ctx->order_list = nullptr;
+  if (ctx->opt.nranks == 1) {
+    if (!ctx->order_h.empty()) {
+      KPM_CUDA(cudaMalloc(&ctx->order_list, sizeof(int64_t) * n));
+      KPM_CUDA(cudaMemcpy(ctx->order_list, ord.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+    }
+    return KPM_OK;
+  }
+  std::vector<int64_t> edge, interior;
+  for (int64_t c : ord) (ctx->edge_flag[c] ? edge : interior).push_back(c);
+  ctx->n_edge = (int64_t)edge.size();
+  ctx->n_interior = (int64_t)interior.size();
   if (!edge.empty())
     KPM_CUDA(cudaMemcpy(ctx->edge_list, edge.data(), sizeof(int64_t) * edge.size(), cudaMemcpyHostToDevice));
   if (!interior.empty())
     KPM_CUDA(cudaMemcpy(ctx->interior_list, interior.data(), sizeof(int64_t) * interior.size(), cudaMemcpyHostToDevice));
-  if (!hs.halo.empty())
-    KPM_CUDA(cudaMemcpy(ctx->halo_rows, hs.halo.data(), sizeof(int64_t) * hs.halo.size(), cudaMemcpyHostToDevice));
   return KPM_OK;
+}
+
+extern "C" kpm_status kpm_set_chunk_order(kpm_ctx* ctx, const int64_t* order, int64_t n) {
+  if (!ctx) return KPM_EINVAL;
+  if (ctx->sticky) return fail(ctx, KPM_ESTATE, "context has a sticky CUDA/NCCL error: " + ctx->err);
+  if (!ctx->have_matrix) return fail(ctx, KPM_ESTATE, "kpm_set_matrix has not been called");
+  KPM_CUDA(cudaSetDevice(ctx->opt.device));
+  if (!order) {
+    ctx->order_h.clear();
+    return apply_order(ctx);
+  }
+  if (n != ctx->sell.n_chunks) return fail(ctx, KPM_EINVAL, "order must list every chunk once");
+  std::vector<char> seen(n, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    if (order[i] < 0 || order[i] >= n || seen[order[i]]) return fail(ctx, KPM_EINVAL, "order is not a permutation");
+    seen[order[i]] = 1;
+  }
+  ctx->order_h.assign(order, order + n);
+  return apply_order(ctx);
 }
 
 // After a sweep: owners' new rows of X -> the neighbours' halo slots of X (grouped NCCL P2P).
@@ -447,11 +495,15 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
   ctx->edge_list = ctx->interior_list = ctx->halo_rows = nullptr;
   ctx->n_edge = 0;
   ctx->n_interior = d.n_chunks;
+  cudaFree(ctx->order_list);
+  ctx->order_list = nullptr;
   ctx->fused = false;
   ctx->fused_ready = false;
+  ctx->order_h.clear();
   if (ctx->opt.nranks > 1) {
     kpm_status st1 = plan_exchange(ctx, hs);
     if (st1 != KPM_OK) return st1;
+    if ((st1 = apply_order(ctx)) != KPM_OK) return st1;
     const char* mode = getenv("KPM_HALO");
     ctx->fused = !(mode && std::string(mode) == "nccl") && ctx->send_runs.size() <= (size_t)kMaxPeerRuns &&
                  load_stream_memops();
@@ -683,7 +735,7 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   sa.col = s.col;
   sa.cptr = s.cptr;
   sa.n_loc = s.n_loc;
-  sa.chunk_list = nullptr;
+  sa.chunk_list = ctx->order_list;  // NULL: storage order
   sa.chunk_begin = 0;
   sa.chunk_end = s.n_chunks;
   sa.rec = s.rec[rec_index];
@@ -692,6 +744,7 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   sa.b = ctx->b;
   sa.pstride = (int64_t)grid * parts;
   sa.n_peer = 0;
+  sa.v_evict_last = env_int("KPM_V_EVICT_LAST", 1);
   // One sweep m (m = 0: init sweep W = a(H - b)V; m >= 1: W <- 2a(H - b)V - W), with the
   // fused eta_2m, eta_2m+1 partials.  Multi-rank: edge chunks first, then the new boundary
   // rows go to the neighbours on the comm stream while the interior chunks run (a5).

@@ -62,6 +62,7 @@ struct SweepArgs {
   const uint4* rec;      // kRecSlots per chunk (sell_build.h)
   const uint16_t* lcol;
   TileLayout tl;
+  int v_evict_last;    // tiled feed: L2 evict-last hint on the gathered V rows (env KPM_V_EVICT_LAST, default 1)
   // fused halo exchange (edge launches only; n_peer = 0 otherwise)
   int n_peer;
   PeerRun peer[kMaxPeerRuns];

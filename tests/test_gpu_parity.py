@@ -224,3 +224,24 @@ def test_every_kernel_variant(pkg, R, monkeypatch):
         seen.add(name)
         check(eta, mu, eta_o)
     assert len(seen) >= 2
+
+
+def test_chunk_order_hint(pkg):
+    """kpm_set_chunk_order changes only the rounding of the eta sums; bad orders rejected."""
+    from workloads.ti_lattice import chunk_order_yband
+
+    lat, rp, col, val, a, b = problem((6, 10, 16))
+    M, R = 64, 32
+    eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, SEED)
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        ctx.set_chunk_order(chunk_order_yband(lat, 0, lat.nx, 3))
+        mu, eta = ctx.moments(M, R, SEED)
+        check(eta, mu, eta_o)
+        mu2, _ = ctx.moments(M, R, SEED)
+        assert np.array_equal(mu, mu2)
+        with pytest.raises(pkg.KpmError):
+            ctx.set_chunk_order(np.zeros(ctx.sell_info().n_chunks, dtype=np.int64))
+        ctx.set_chunk_order(None)
+        mu3, eta3 = ctx.moments(M, R, SEED)
+        check(eta3, mu3, eta_o)

@@ -245,6 +245,23 @@ def bloch_energies(lat: Lattice) -> np.ndarray:
     return np.concatenate([e, e, -e, -e])
 
 
+def chunk_order_yband(lat: Lattice, x0: int, x1: int, band: int, C: int = 32):
+    """Locality hint for kpm_set_chunk_order (not method arithmetic): the SELL chunks of the
+    x-slab [x0, x1) (C = 32 rows = 8 sites along z, sigma = 1, Nz % 8 == 0) ordered by y-band,
+    then x, then y, then z-block, so the x-neighbour window a sweep keeps in L2 shrinks from
+    2 x-planes to 2 band-planes."""
+    if (4 * lat.nz) % C:
+        raise ValueError("needs 8 | Nz so chunks align with z-columns")
+    zb = 4 * lat.nz // C
+    order = []
+    for y0 in range(0, lat.ny, band):
+        ys = np.arange(y0, min(y0 + band, lat.ny))
+        for x in range(x1 - x0):
+            base = (x * lat.ny + ys)[:, None] * zb + np.arange(zb)[None, :]
+            order.append(base.ravel())
+    return np.concatenate(order).astype(np.int64)
+
+
 # ---- configurations of BASELINE.json (SURVEY §8(d)) ----------------------------------
 CONFIGS = {
     "C1": dict(lattice=(8, 8, 8), M=64, R=4),
