@@ -23,33 +23,30 @@ std::vector<RecvRun> plan_recv_runs(const std::vector<int64_t>& halo, const std:
 
 bool plan_send_runs(int peer, const std::vector<int64_t>& req, int64_t row_begin, int64_t row_end,
                     const std::vector<int32_t>& perm, std::vector<SendRun>& out) {
-  std::vector<int64_t> invperm(perm.size());
-  for (size_t p = 0; p < perm.size(); ++p) invperm[perm[p]] = (int64_t)p;
+  std::vector<int64_t> invperm;
+  if (!perm.empty()) {
+    invperm.resize(perm.size());
+    for (size_t p = 0; p < perm.size(); ++p) invperm[perm[p]] = (int64_t)p;
+  }
+  auto pos = [&](int64_t g) { return invperm.empty() ? g - row_begin : invperm[g - row_begin]; };
   for (size_t i = 0; i + 1 < req.size(); i += 2) {
     const int64_t g0 = req[i], cnt = req[i + 1];
     if (cnt < 1 || g0 < row_begin || g0 + cnt > row_end) return false;
-    const int64_t p0 = invperm[g0 - row_begin];
+    const int64_t p0 = pos(g0);
     for (int64_t k = 1; k < cnt; ++k)
-      if (invperm[g0 + k - row_begin] != p0 + k) return false;
+      if (pos(g0 + k) != p0 + k) return false;
     out.push_back(SendRun{peer, p0, cnt, -1});
   }
   return true;
 }
 
-void plan_edge_chunks(const std::vector<int64_t>& cptr, const int32_t* col, int64_t n_pad, int C,
-                      const std::vector<SendRun>& sends, std::vector<int64_t>& edge, std::vector<int64_t>& interior) {
-  const int64_t n_chunks = (int64_t)cptr.size() - 1;
+void plan_edge_chunks(int64_t n_chunks, const std::vector<char>& reads_halo, int C, const std::vector<SendRun>& sends,
+                      std::vector<int64_t>& edge, std::vector<int64_t>& interior) {
   std::vector<char> is_edge(n_chunks, 0);
   for (const SendRun& s : sends)
     for (int64_t c = s.pos / C; c <= (s.pos + s.count - 1) / C; ++c) is_edge[c] = 1;
-  for (int64_t c = 0; c < n_chunks; ++c) {
-    if (is_edge[c]) continue;
-    for (int64_t k = cptr[c]; k < cptr[c + 1]; ++k)
-      if (col[k] >= n_pad) {
-        is_edge[c] = 1;
-        break;
-      }
-  }
+  for (int64_t c = 0; c < n_chunks && c < (int64_t)reads_halo.size(); ++c)
+    if (reads_halo[c]) is_edge[c] = 1;
   edge.clear();
   interior.clear();
   for (int64_t c = 0; c < n_chunks; ++c) (is_edge[c] ? edge : interior).push_back(c);

@@ -29,14 +29,14 @@ struct SendRun {
 std::vector<RecvRun> plan_recv_runs(const std::vector<int64_t>& halo, const std::vector<int64_t>& row_begins);
 
 // Send runs for the runs `req` (gfirst, count pairs, in the requester's order) that `peer`
-// asked of this rank.  pos = invperm[g - row_begin]; every requested run must map to
-// consecutive positions (true for sigma = 1), otherwise returns false.
+// asked of this rank.  pos = invperm[g - row_begin] (perm empty = identity); every requested
+// run must map to consecutive positions (true for sigma = 1), otherwise returns false.
 bool plan_send_runs(int peer, const std::vector<int64_t>& req, int64_t row_begin, int64_t row_end,
                     const std::vector<int32_t>& perm, std::vector<SendRun>& out);
 
 // Chunks that must be computed before the exchange (they hold rows that are sent) or that
-// read halo slots; the rest are interior.  Both lists ascending.
-void plan_edge_chunks(const std::vector<int64_t>& cptr, const int32_t* col, int64_t n_pad, int C,
-                      const std::vector<SendRun>& sends, std::vector<int64_t>& edge, std::vector<int64_t>& interior);
+// read halo slots (reads_halo[c], empty = none); the rest are interior.  Both ascending.
+void plan_edge_chunks(int64_t n_chunks, const std::vector<char>& reads_halo, int C, const std::vector<SendRun>& sends,
+                      std::vector<int64_t>& edge, std::vector<int64_t>& interior);
 
 }  // namespace kpm

@@ -43,8 +43,7 @@ struct kpm_ctx {
   double a = 0.0, b = 0.0;
   DevSell sell;
   std::vector<int64_t> halo;  // global ids of halo slots
-  HostTiles tiles;            // runs of the tiled feed (host copy, for the per-R records)
-  std::vector<int64_t> cptr_h;
+  std::vector<int64_t> cptr_h;  // host copy of cptr
 
   // work buffers (grow-only)
   double2* X0 = nullptr;
@@ -243,16 +242,19 @@ static void free_sell(DevSell& s) {
   cudaFree(s.cptr);
   cudaFree(s.perm);
   cudaFree(s.lcol);
+  cudaFree(s.nruns);
+  cudaFree(s.runs);
   for (int i = 0; i < 12; ++i) cudaFree(s.rec[i]);
   s = DevSell();
 }
 
 // Halo exchange plan (collective): receive runs from the halo list, requests to the owners,
 // send runs from the requests, edge / interior chunk split (halo_plan.h).
-static kpm_status plan_exchange(kpm_ctx* ctx, const HostSell& hs) {
+static kpm_status plan_exchange(kpm_ctx* ctx, const std::vector<int64_t>& halo, int64_t n_pad,
+                                const std::vector<int32_t>& perm, const std::vector<char>& reads_halo) {
   const int P = ctx->opt.nranks, me = ctx->opt.rank;
   const int64_t row_begin = ctx->row_begins[me], row_end = ctx->row_begins[me + 1];
-  ctx->recv_runs = plan_recv_runs(hs.halo, ctx->row_begins);
+  ctx->recv_runs = plan_recv_runs(halo, ctx->row_begins);
   // requests: per owner q the (gfirst, count) pairs, in slot order
   std::vector<std::vector<int64_t>> req(P);
   for (const RecvRun& r : ctx->recv_runs) {  // (first global row, count, first halo slot)
@@ -302,19 +304,19 @@ static kpm_status plan_exchange(kpm_ctx* ctx, const HostSell& hs) {
     }
     off += n;
     const size_t first = ctx->send_runs.size();
-    if (!plan_send_runs(p, rq, row_begin, row_end, hs.perm, ctx->send_runs))
+    if (!plan_send_runs(p, rq, row_begin, row_end, perm, ctx->send_runs))
       return fail(ctx, KPM_EINVAL, "halo request does not map to contiguous local rows");
     for (size_t i = first; i < ctx->send_runs.size(); ++i) ctx->send_runs[i].peer_slot = slots[i - first];
   }
   std::vector<int64_t> edge, interior;
-  plan_edge_chunks(hs.cptr, hs.col.data(), hs.n_pad, hs.C, ctx->send_runs, edge, interior);
-  ctx->edge_flag.assign(hs.n_chunks, 0);
+  plan_edge_chunks((int64_t)ctx->cptr_h.size() - 1, reads_halo, kC, ctx->send_runs, edge, interior);
+  ctx->edge_flag.assign(ctx->cptr_h.size() - 1, 0);
   for (int64_t c : edge) ctx->edge_flag[c] = 1;
   KPM_CUDA(cudaMalloc(&ctx->edge_list, sizeof(int64_t) * std::max<size_t>(1, edge.size())));
   KPM_CUDA(cudaMalloc(&ctx->interior_list, sizeof(int64_t) * std::max<size_t>(1, interior.size())));
-  KPM_CUDA(cudaMalloc(&ctx->halo_rows, sizeof(int64_t) * std::max<size_t>(1, hs.halo.size())));
-  if (!hs.halo.empty())
-    KPM_CUDA(cudaMemcpy(ctx->halo_rows, hs.halo.data(), sizeof(int64_t) * hs.halo.size(), cudaMemcpyHostToDevice));
+  KPM_CUDA(cudaMalloc(&ctx->halo_rows, sizeof(int64_t) * std::max<size_t>(1, halo.size())));
+  if (!halo.empty())
+    KPM_CUDA(cudaMemcpy(ctx->halo_rows, halo.data(), sizeof(int64_t) * halo.size(), cudaMemcpyHostToDevice));
   return KPM_OK;
 }
 
@@ -405,87 +407,128 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
     if (row_begins.back() != H->n_global) return fail(ctx, KPM_EINVAL, "row ranges do not cover n_global");
   }
 
-  // host views of the CSR (device input is staged through the host for the build)
-  std::vector<int64_t> rp_h, col_h;
-  std::vector<double> val_h;
-  const int64_t* rp = H->row_ptr;
-  const int64_t* col = H->col;
-  const double* val = H->val;
-  if (H->mem == KPM_MEM_DEVICE) {
-    rp_h.resize(n_loc + 1);
-    KPM_CUDA(cudaMemcpy(rp_h.data(), H->row_ptr, sizeof(int64_t) * (n_loc + 1), cudaMemcpyDeviceToHost));
-    const int64_t nnz = rp_h[n_loc];
-    if (nnz < 0) return fail(ctx, KPM_EINVAL, "malformed row_ptr");
-    col_h.resize(nnz);
-    val_h.resize(2 * nnz);
-    KPM_CUDA(cudaMemcpy(col_h.data(), H->col, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
-    KPM_CUDA(cudaMemcpy(val_h.data(), H->val, sizeof(double) * 2 * nnz, cudaMemcpyDeviceToHost));
-    rp = rp_h.data();
-    col = col_h.data();
-    val = val_h.data();
-  }
-  if (rp[0] != 0) return fail(ctx, KPM_EINVAL, "row_ptr[0] != 0");
-  for (int64_t i = 0; i < n_loc; ++i)
-    if (rp[i + 1] < rp[i]) return fail(ctx, KPM_EINVAL, "row_ptr not non-decreasing");
-  const int64_t nnz = rp[n_loc];
-  for (int64_t k = 0; k < nnz; ++k) {
-    if (col[k] < 0 || col[k] >= H->n_global) return fail(ctx, KPM_ERANGE, "column outside [0, n_global)");
-    if (!std::isfinite(val[2 * k]) || !std::isfinite(val[2 * k + 1])) return fail(ctx, KPM_EINVAL, "non-finite value");
-  }
-
-  HostSell hs;
-  std::string berr;
-  int st = build_sell_host(rp, col, val, n_loc, H->row_begin, H->row_end, ctx->opt.sell_C, ctx->opt.sell_sigma, hs,
-                           berr);
-  if (st) return fail(ctx, (kpm_status)st, berr);
-  if (ctx->opt.nranks == 1 && hs.n_halo != 0) return fail(ctx, KPM_EINVAL, "internal: halo on a single rank");
-  ctx->row_begins = row_begins;
-
-  // upload
   free_sell(ctx->sell);
   ctx->have_matrix = false;
   DevSell& d = ctx->sell;
-  d.n_loc = hs.n_loc;
-  d.n_pad = hs.n_pad;
-  d.n_chunks = hs.n_chunks;
-  d.n_slots = hs.cptr[hs.n_chunks];
-  d.n_halo = hs.n_halo;
-  d.max_width = 0;
-  for (int64_t c = 0; c < hs.n_chunks; ++c) d.max_width = std::max(d.max_width, (hs.cptr[c + 1] - hs.cptr[c]) / hs.C);
+  std::vector<int64_t> halo;       // global ids of the halo slots
+  std::vector<int32_t> perm_h;     // host perm (empty = identity)
+  std::vector<char> reads_halo;    // per chunk, multi-rank planning
   auto alloc = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
-  cudaError_t e = alloc((void**)&d.val, sizeof(double2) * d.n_slots);
-  if (e == cudaSuccess) e = alloc((void**)&d.col, sizeof(int) * d.n_slots);
-  if (e == cudaSuccess) e = alloc((void**)&d.cptr, sizeof(int64_t) * (d.n_chunks + 1));
-  if (e == cudaSuccess) e = alloc((void**)&d.perm, sizeof(int) * d.n_loc);
-  if (e != cudaSuccess) {
-    free_sell(ctx->sell);
-    cudaGetLastError();
-    return fail(ctx, KPM_ENOMEM, std::string("device allocation for the matrix failed: ") + cudaGetErrorString(e));
-  }
-  KPM_CUDA(cudaMemcpy(d.val, hs.val.data(), sizeof(double2) * d.n_slots, cudaMemcpyHostToDevice));
-  KPM_CUDA(cudaMemcpy(d.col, hs.col.data(), sizeof(int) * d.n_slots, cudaMemcpyHostToDevice));
-  KPM_CUDA(cudaMemcpy(d.cptr, hs.cptr.data(), sizeof(int64_t) * (d.n_chunks + 1), cudaMemcpyHostToDevice));
-  KPM_CUDA(cudaMemcpy(d.perm, hs.perm.data(), sizeof(int) * d.n_loc, cudaMemcpyHostToDevice));
-  // gather plan of the tiled feed (copy records are built per block width on first use)
-  {
-    build_tiles_host(hs, ctx->tiles);
-    d.tiles_ok = ctx->tiles.ok;
-    d.max_other = ctx->tiles.max_other;
-    d.max_runs = ctx->tiles.max_runs;
-    ctx->cptr_h = hs.cptr;
+
+  if (H->mem == KPM_MEM_DEVICE && ctx->opt.sell_sigma == 1) {
+    // device build: the CSR never leaves the GPU (sell_device.cu)
+    DeviceBuild db;
+    std::string berr;
+    const int st = build_sell_device(H->row_ptr, H->col, reinterpret_cast<const double2*>(H->val), n_loc,
+                                     H->row_begin, H->row_end, H->n_global, d, db, berr, ctx->stream);
+    if (st) {
+      free_sell(ctx->sell);
+      cudaGetLastError();
+      if (st == 5) {
+        ctx->sticky = true;
+        return fail(ctx, KPM_ECUDA, berr);
+      }
+      return fail(ctx, (kpm_status)st, berr);
+    }
+    halo = std::move(db.halo);
+    reads_halo = std::move(db.reads_halo);
+    ctx->cptr_h = std::move(db.cptr);
+  } else {
+    // host build (device input is staged through the host)
+    std::vector<int64_t> rp_h, col_h;
+    std::vector<double> val_h;
+    const int64_t* rp = H->row_ptr;
+    const int64_t* col = H->col;
+    const double* val = H->val;
+    if (H->mem == KPM_MEM_DEVICE) {
+      rp_h.resize(n_loc + 1);
+      KPM_CUDA(cudaMemcpy(rp_h.data(), H->row_ptr, sizeof(int64_t) * (n_loc + 1), cudaMemcpyDeviceToHost));
+      const int64_t nnz = rp_h[n_loc];
+      if (nnz < 0) return fail(ctx, KPM_EINVAL, "malformed row_ptr");
+      col_h.resize(nnz);
+      val_h.resize(2 * nnz);
+      KPM_CUDA(cudaMemcpy(col_h.data(), H->col, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
+      KPM_CUDA(cudaMemcpy(val_h.data(), H->val, sizeof(double) * 2 * nnz, cudaMemcpyDeviceToHost));
+      rp = rp_h.data();
+      col = col_h.data();
+      val = val_h.data();
+    }
+    if (rp[0] != 0) return fail(ctx, KPM_EINVAL, "row_ptr[0] != 0");
+    for (int64_t i = 0; i < n_loc; ++i)
+      if (rp[i + 1] < rp[i]) return fail(ctx, KPM_EINVAL, "row_ptr not non-decreasing");
+    const int64_t nnz = rp[n_loc];
+    for (int64_t k = 0; k < nnz; ++k) {
+      if (col[k] < 0 || col[k] >= H->n_global) return fail(ctx, KPM_ERANGE, "column outside [0, n_global)");
+      if (!std::isfinite(val[2 * k]) || !std::isfinite(val[2 * k + 1])) return fail(ctx, KPM_EINVAL, "non-finite value");
+    }
+    HostSell hs;
+    std::string berr;
+    int st = build_sell_host(rp, col, val, n_loc, H->row_begin, H->row_end, ctx->opt.sell_C, ctx->opt.sell_sigma, hs,
+                             berr);
+    if (st) return fail(ctx, (kpm_status)st, berr);
+    d.n_loc = hs.n_loc;
+    d.n_pad = hs.n_pad;
+    d.n_chunks = hs.n_chunks;
+    d.n_slots = hs.cptr[hs.n_chunks];
+    d.n_halo = hs.n_halo;
+    d.max_width = 0;
+    for (int64_t c = 0; c < hs.n_chunks; ++c) d.max_width = std::max(d.max_width, (hs.cptr[c + 1] - hs.cptr[c]) / hs.C);
+    cudaError_t e = alloc((void**)&d.val, sizeof(double2) * d.n_slots);
+    if (e == cudaSuccess) e = alloc((void**)&d.col, sizeof(int) * d.n_slots);
+    if (e == cudaSuccess) e = alloc((void**)&d.cptr, sizeof(int64_t) * (d.n_chunks + 1));
+    if (e == cudaSuccess && hs.sigma > 1) e = alloc((void**)&d.perm, sizeof(int) * d.n_loc);
+    if (e != cudaSuccess) {
+      free_sell(ctx->sell);
+      cudaGetLastError();
+      return fail(ctx, KPM_ENOMEM, std::string("device allocation for the matrix failed: ") + cudaGetErrorString(e));
+    }
+    KPM_CUDA(cudaMemcpy(d.val, hs.val.data(), sizeof(double2) * d.n_slots, cudaMemcpyHostToDevice));
+    KPM_CUDA(cudaMemcpy(d.col, hs.col.data(), sizeof(int) * d.n_slots, cudaMemcpyHostToDevice));
+    KPM_CUDA(cudaMemcpy(d.cptr, hs.cptr.data(), sizeof(int64_t) * (d.n_chunks + 1), cudaMemcpyHostToDevice));
+    if (d.perm) {
+      KPM_CUDA(cudaMemcpy(d.perm, hs.perm.data(), sizeof(int) * d.n_loc, cudaMemcpyHostToDevice));
+      perm_h = hs.perm;
+    }
+    // gather plan of the tiled feed: lcol + fixed-capacity run lists (records per R on use)
+    HostTiles t;
+    build_tiles_host(hs, t);
+    d.tiles_ok = t.ok && t.max_runs <= kMaxRuns;
+    d.max_other = t.max_other;
+    d.max_runs = t.max_runs;
     if (d.tiles_ok) {
-      if (alloc((void**)&d.lcol, sizeof(uint16_t) * ctx->tiles.lcol.size()) != cudaSuccess) {
+      std::vector<int> nr(d.n_chunks), rr((size_t)2 * kMaxRuns * d.n_chunks, 0);
+      for (int64_t c = 0; c < d.n_chunks; ++c) {
+        nr[c] = (int)(t.run_ptr[c + 1] - t.run_ptr[c]);
+        for (int64_t k = t.run_ptr[c]; k < t.run_ptr[c + 1]; ++k) {
+          rr[c * 2 * kMaxRuns + 2 * (k - t.run_ptr[c])] = t.runs[2 * k];
+          rr[c * 2 * kMaxRuns + 2 * (k - t.run_ptr[c]) + 1] = t.runs[2 * k + 1];
+        }
+      }
+      if (alloc((void**)&d.lcol, sizeof(uint16_t) * t.lcol.size()) != cudaSuccess ||
+          alloc((void**)&d.nruns, sizeof(int) * nr.size()) != cudaSuccess ||
+          alloc((void**)&d.runs, sizeof(int) * rr.size()) != cudaSuccess) {
         cudaGetLastError();
-        d.lcol = nullptr;
         d.tiles_ok = false;  // the other feeds still work
       } else {
-        KPM_CUDA(cudaMemcpy(d.lcol, ctx->tiles.lcol.data(), sizeof(uint16_t) * ctx->tiles.lcol.size(),
-                            cudaMemcpyHostToDevice));
+        KPM_CUDA(cudaMemcpy(d.lcol, t.lcol.data(), sizeof(uint16_t) * t.lcol.size(), cudaMemcpyHostToDevice));
+        KPM_CUDA(cudaMemcpy(d.nruns, nr.data(), sizeof(int) * nr.size(), cudaMemcpyHostToDevice));
+        KPM_CUDA(cudaMemcpy(d.runs, rr.data(), sizeof(int) * rr.size(), cudaMemcpyHostToDevice));
       }
     }
-    raw_vector<uint16_t>().swap(ctx->tiles.lcol);  // host copy no longer needed
+    halo = hs.halo;
+    ctx->cptr_h = hs.cptr;
+    if (!halo.empty()) {
+      reads_halo.assign(d.n_chunks, 0);
+      for (int64_t c = 0; c < d.n_chunks; ++c)
+        for (int64_t k = hs.cptr[c]; k < hs.cptr[c + 1]; ++k)
+          if (hs.col[k] >= hs.n_pad) {
+            reads_halo[c] = 1;
+            break;
+          }
+    }
   }
-  ctx->halo = hs.halo;
+  if (ctx->opt.nranks == 1 && d.n_halo != 0) return fail(ctx, KPM_EINVAL, "internal: halo on a single rank");
+  ctx->halo = halo;
   ctx->row_begins = row_begins;
   ctx->recv_runs.clear();
   ctx->send_runs.clear();
@@ -501,7 +544,7 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
   ctx->fused_ready = false;
   ctx->order_h.clear();
   if (ctx->opt.nranks > 1) {
-    kpm_status st1 = plan_exchange(ctx, hs);
+    kpm_status st1 = plan_exchange(ctx, halo, d.n_pad, perm_h, reads_halo);
     if (st1 != KPM_OK) return st1;
     if ((st1 = apply_order(ctx)) != KPM_OK) return st1;
     const char* mode = getenv("KPM_HALO");
@@ -661,15 +704,15 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     plan = s.tiles_ok ? plan_tiles(Rk, s.max_other, s.max_width, std::min(ctx->tile_stages, 4), with_w) : TileLayout();
     const int ri = 2 * lg + (with_w ? 1 : 0);
     if (plan.stages >= 1 && !ctx->sell.rec[ri] && !ctx->sell.rec_failed[ri]) {
-      std::vector<uint32_t> rec;
-      if (!build_tile_records(ctx->cptr_h, ctx->tiles, Rk, plan.off_w, plan.off_val, plan.off_lcol, rec)) {
-        ctx->sell.rec_failed[ri] = true;
-      } else {
-        size_t cap = 0;
-        kpm_status st2 = ensure(ctx, (void**)&ctx->sell.rec[ri], &cap, rec.size() / 4, sizeof(uint4));
-        if (st2 != KPM_OK) return st2;
-        KPM_CUDA(cudaMemcpy(ctx->sell.rec[ri], rec.data(), sizeof(uint32_t) * rec.size(), cudaMemcpyHostToDevice));
+      size_t cap = 0;
+      kpm_status st2 = ensure(ctx, (void**)&ctx->sell.rec[ri], &cap, (size_t)kRecSlots * s.n_chunks, sizeof(uint4));
+      if (st2 != KPM_OK) {
+        ctx->sell.rec_failed[ri] = true;  // no memory for the records: another feed runs
+        plan = TileLayout();
+        return KPM_OK;
       }
+      KPM_CUDA(launch_build_records(s.cptr, s.nruns, s.runs, s.n_chunks, Rk, plan.off_w, plan.off_val, plan.off_lcol,
+                                    ctx->sell.rec[ri], ctx->stream));
     }
     if (!ctx->sell.rec[ri]) plan = TileLayout();
     return KPM_OK;
@@ -937,7 +980,9 @@ extern "C" kpm_status kpm_export_sell(const kpm_ctx* ctx_c, double* val, int32_t
   if (val) KPM_CUDA(cudaMemcpy(val, s.val, sizeof(double2) * s.n_slots, cudaMemcpyDeviceToHost));
   if (col) KPM_CUDA(cudaMemcpy(col, s.col, sizeof(int) * s.n_slots, cudaMemcpyDeviceToHost));
   if (cptr) KPM_CUDA(cudaMemcpy(cptr, s.cptr, sizeof(int64_t) * (s.n_chunks + 1), cudaMemcpyDeviceToHost));
-  if (perm) KPM_CUDA(cudaMemcpy(perm, s.perm, sizeof(int) * s.n_loc, cudaMemcpyDeviceToHost));
+  if (perm && s.perm) KPM_CUDA(cudaMemcpy(perm, s.perm, sizeof(int) * s.n_loc, cudaMemcpyDeviceToHost));
+  if (perm && !s.perm)
+    for (int64_t p = 0; p < s.n_loc; ++p) perm[p] = (int32_t)p;  // sigma = 1: identity
   if (halo && !ctx->halo.empty()) std::memcpy(halo, ctx->halo.data(), sizeof(int64_t) * ctx->halo.size());
   return KPM_OK;
 }

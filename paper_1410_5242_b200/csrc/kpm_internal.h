@@ -12,18 +12,22 @@ namespace kpm {
 constexpr int kC = 32;             // SELL chunk height = warpSize (north_star subsystem 1)
 constexpr int kThreads = 256;      // threads per CTA of the sweep kernels (8 warps)
 constexpr int kMaxBlockWidth = 32; // widest specialised block (R per batch)
+constexpr int kRecSlots = 16;      // copy-record slots per chunk (header + 15 bulk copies)
+constexpr int kMaxRuns = kRecSlots - 5;  // row runs per chunk (besides own rows, W, val, lcol)
 
 // Device-side SELL-C-sigma matrix ("Data layout in HBM").
 struct DevSell {
   double2* val = nullptr;  // n_slots, chunk-column-major: entry j of row k of chunk c at cptr[c]+j*32+k
   int* col = nullptr;      // n_slots, int32 local column (position in the local+halo vector)
   int64_t* cptr = nullptr; // n_chunks+1
-  int* perm = nullptr;     // n_loc: local row stored at position p
+  int* perm = nullptr;     // n_loc: local row stored at position p (NULL: identity, sigma = 1)
   int64_t n_loc = 0, n_pad = 0, n_chunks = 0, n_slots = 0, n_halo = 0;
   int64_t max_width = 0;   // widest chunk (entries per row)
   // tiled feed (TMA gather plan, see sell_build.h HostTiles)
   bool tiles_ok = false;
   uint16_t* lcol = nullptr;    // n_slots: column as index into the chunk's shared-memory tile
+  int* nruns = nullptr;        // n_chunks: runs of other rows per chunk
+  int* runs = nullptr;         // n_chunks x kMaxRuns x (first row, count)
   int64_t max_other = 0, max_runs = 0;
   uint4* rec[12] = {};        // copy records per (log2(R), W staged)
   bool rec_failed[12] = {};
@@ -91,5 +95,17 @@ cudaError_t launch_aug_spmmv(int R, int variant, bool init, const SweepArgs& a, 
 // eta[m][r] (double2) for m in [0, n_sweeps) from partials[m][3R][width] (width = launches x grid)
 cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int width, double2* eta_even,
                                 double2* eta_odd, cudaStream_t s);
+
+// Device-side setup (sell_device.cu): CSR on the device -> SELL-32 (sigma = 1) + tile plan.
+struct DeviceBuild {
+  std::vector<int64_t> halo;     // global ids of the halo slots (host copy)
+  std::vector<int64_t> cptr;     // host copy of cptr
+  std::vector<char> reads_halo;  // per chunk (empty if no halo)
+};
+int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val, int64_t n_loc, int64_t row_begin,
+                      int64_t row_end, int64_t n_global, DevSell& d, DeviceBuild& out, std::string& err, cudaStream_t s);
+// Copy records of the tiled feed for block width R from the per-chunk run lists.
+cudaError_t launch_build_records(const int64_t* cptr, const int* nruns, const int* runs, int64_t n_chunks, int R,
+                                 int off_w, int off_val, int off_lcol, uint4* rec, cudaStream_t s);
 
 }  // namespace kpm

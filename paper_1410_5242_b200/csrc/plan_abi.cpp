@@ -40,8 +40,7 @@ extern "C" kpm_status kpm_plan_recv(int nranks, const int64_t* row_begins, int r
 extern "C" kpm_status kpm_plan_send(int64_t row_begin, int64_t row_end, int peer, int64_t n_req, const int64_t* req,
                                     int64_t* n_runs, int64_t* runs) {
   if (row_end < row_begin || n_req < 0 || (n_req && !req) || !n_runs) return KPM_EINVAL;
-  std::vector<int32_t> perm(row_end - row_begin);
-  for (size_t p = 0; p < perm.size(); ++p) perm[p] = (int32_t)p;  // sigma = 1
+  const std::vector<int32_t> perm;  // sigma = 1: identity
   std::vector<int64_t> rq(req, req + 2 * n_req);
   std::vector<SendRun> out;
   if (!plan_send_runs(peer, rq, row_begin, row_end, perm, out)) return KPM_ERANGE;

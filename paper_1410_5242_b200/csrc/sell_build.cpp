@@ -181,47 +181,4 @@ void build_tiles_host(const HostSell& s, HostTiles& out) {
   }
 }
 
-bool build_tile_records(const std::vector<int64_t>& cptr, const HostTiles& t, int R, int off_w, int off_val,
-                        int off_lcol, std::vector<uint32_t>& rec) {
-  const int64_t n_chunks = (int64_t)cptr.size() - 1;
-  const int64_t rowb = (int64_t)R * 16;
-  const int C = 32;
-  rec.assign((size_t)n_chunks * kRecSlots * 4, 0u);
-  for (int64_t c = 0; c < n_chunks; ++c) {
-    uint32_t* r = rec.data() + (size_t)c * kRecSlots * 4;
-    int n = 0;
-    int64_t total = 0, wbytes = 0;
-    auto cmd = [&](int base, int64_t src, int64_t dst, int64_t bytes) {
-      ++n;
-      if (n >= kRecSlots) return;
-      uint32_t* q = r + 4 * n;
-      q[0] = (uint32_t)src;
-      q[1] = (uint32_t)((uint64_t)src >> 32);
-      q[2] = (uint32_t)dst;
-      q[3] = (uint32_t)bytes | ((uint32_t)base << 28);
-      total += bytes;
-    };
-    const int64_t s0 = cptr[c], nslot = cptr[c + 1] - cptr[c];
-    cmd(0, c * C * rowb, 0, C * rowb);
-    cmd(1, c * C * rowb, off_w, C * rowb);
-    wbytes = C * rowb;
-    if (nslot) {
-      cmd(2, s0 * 16, off_val, nslot * 16);
-      cmd(3, s0 * 2, off_lcol, nslot * 2);
-    }
-    int64_t dst_row = C;
-    for (int64_t k = t.run_ptr[c]; k < t.run_ptr[c + 1]; ++k) {
-      const int64_t first = t.runs[2 * k], cnt = t.runs[2 * k + 1];
-      cmd(0, first * rowb, dst_row * rowb, cnt * rowb);
-      dst_row += cnt;
-    }
-    if (n >= kRecSlots) return false;
-    r[0] = (uint32_t)total;
-    r[1] = (uint32_t)(total - wbytes);
-    r[2] = (uint32_t)(nslot / C);
-    r[3] = (uint32_t)n;
-  }
-  return true;
-}
-
 }  // namespace kpm

@@ -55,13 +55,10 @@ struct HostTiles {
 };
 void build_tiles_host(const HostSell& s, HostTiles& out);
 
-// Copy-command records of the tiled feed for block width R: 16 x 16-byte slots per chunk.
-// Slot 0 = {bytes (main sweep), bytes (init sweep, no W), chunk width L, n_cmd}; slots
-// 1..n_cmd = {src byte offset lo, hi, dst byte offset in the stage, bytes | base << 28} with
-// base 0 = V, 1 = W, 2 = val, 3 = lcol.  Returns false if a chunk needs more than 15 copies.
-constexpr int kRecSlots = 16;
-bool build_tile_records(const std::vector<int64_t>& cptr, const HostTiles& t, int R, int off_w, int off_val,
-                        int off_lcol, std::vector<uint32_t>& rec);
+// Copy-command records of the tiled feed (built on the device, sell_device.cu): kRecSlots x
+// 16-byte slots per chunk.  Slot 0 = {bytes (main sweep), bytes (init sweep, no W), chunk
+// width L, n_cmd}; slots 1..n_cmd = {src byte offset lo, hi, dst byte offset in the stage,
+// bytes | base << 28} with base 0 = V, 1 = W, 2 = val, 3 = lcol.
 
 // Returns 0 or a kpm_status code (err filled).
 int build_sell_host(const int64_t* row_ptr, const int64_t* col, const double* val, int64_t n_loc,

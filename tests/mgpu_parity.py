@@ -28,7 +28,8 @@ def main():
     uid = [kpm.get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     results, mu_by_case = {}, {}
-    cases = [((8, 8, 8), 64, 4, SEED), ((12, 5, 8), 80, 32, 7), ((10, 3, 5), 40, 5, 11), ((6, 4, 16), 200, 16, 3)]
+    cases = [((8, 8, 8), 64, 4, SEED), ((12, 5, 8), 80, 32, 7), ((10, 3, 5), 40, 5, 11), ((6, 4, 16), 200, 16, 3),
+             ((12, 6, 16), 60, 32, "device")]
     ctx = kpm.KpmContext(device=local, nranks=world, rank=rank, nccl_unique_id=uid[0])
     for (dims, M, R, seed), mode in [(c, m) for m in ("fused", "nccl") for c in cases]:
         os.environ["KPM_HALO"] = mode  # read by kpm_set_matrix
@@ -36,8 +37,16 @@ def main():
         planes = [lat.nx * q // world for q in range(world + 1)]
         rp_g, col_g, val_g = generate_csr(lat)
         a, b = scale_factors(*gershgorin(rp_g, col_g, val_g))
-        rp, col, val = generate_csr(lat, planes[rank], planes[rank + 1])
-        ctx.set_matrix(rp, col, val, a, b, n_global=lat.n, row_begin=planes[rank] * lat.rows_per_plane)
+        if seed == "device":  # CSR generated and converted on the GPU (KPM_MEM_DEVICE)
+            from workloads.ti_lattice import generate_csr_torch
+
+            seed = 13
+            rp, col, val = generate_csr_torch(lat, planes[rank], planes[rank + 1], device=f"cuda:{local}")
+            ctx.set_matrix(rp, col, val, a, b, n_global=lat.n, row_begin=planes[rank] * lat.rows_per_plane,
+                           mem=kpm.KPM_MEM_DEVICE)
+        else:
+            rp, col, val = generate_csr(lat, planes[rank], planes[rank + 1])
+            ctx.set_matrix(rp, col, val, a, b, n_global=lat.n, row_begin=planes[rank] * lat.rows_per_plane)
         mu, eta = ctx.moments(M, R, seed)
         if mode == "fused":
             mu_by_case[dims] = mu

@@ -204,6 +204,52 @@ def generate_csr(lat: Lattice, x0: int = 0, x1: int | None = None):
     return row_ptr, col, val
 
 
+def generate_csr_torch(lat: Lattice, x0: int = 0, x1: int | None = None, device="cpu", batch: int = 64):
+    """The same CSR as generate_csr (identical entry order and values), built with torch on
+    `device` -- for slabs too large to stage through host memory (C5: 1.5e9 nonzeros per GPU).
+    Every x-plane repeats the plane template of x = 1 (neighbour planes 0, 1, 2), shifted by x
+    with periodic wrap; only the diagonal potential depends on x."""
+    import torch
+
+    if x1 is None:
+        x1 = lat.nx
+    if lat.nx < 3:
+        raise ValueError("generate_csr_torch needs Nx >= 3")
+    P = lat.rows_per_plane
+    zero = Lattice(lat.nx, lat.ny, lat.nz, potential=ZERO_POTENTIAL, periodic_z=lat.periodic_z)
+    rp1, col1, val1 = generate_csr(zero, 1, 2)
+    dx = col1 // P - 1  # -1, 0, +1
+    rloc = col1 % P
+    rows1 = np.repeat(np.arange(P), np.diff(rp1))
+    diag = np.nonzero((dx == 0) & (rloc == rows1))[0]
+    # potential of the plane's diagonal slots as a function of x (x mod S_x < D_x or not)
+    pot = lat.potential
+    y_of = (rows1[diag] // 4) // lat.nz
+    z_of = (rows1[diag] // 4) % lat.nz
+    vdot = np.where(((y_of % pot.spacing[1]) < pot.dot[1]) & (z_of == lat.nz - 1), pot.depth, 0.0)
+    t = lambda a, dt=None: torch.as_tensor(a, device=device, dtype=dt)  # noqa: E731
+    dx_t, rloc_t, val_t = t(dx), t(rloc), t(val1)
+    diag_t, vdot_t = t(diag), t(vdot, torch.float64)
+    nnz_p = len(col1)
+    nplanes = x1 - x0
+    row_ptr = torch.empty(nplanes * P + 1, dtype=torch.int64, device=device)
+    row_ptr[0] = 0
+    lens = t(np.diff(rp1)).repeat(nplanes)
+    torch.cumsum(lens, 0, out=row_ptr[1:])
+    col = torch.empty(nplanes * nnz_p, dtype=torch.int64, device=device)
+    val = torch.empty(nplanes * nnz_p, dtype=torch.complex128, device=device)
+    for b0 in range(0, nplanes, batch):
+        xs = torch.arange(x0 + b0, min(x0 + b0 + batch, x1), device=device, dtype=torch.int64)
+        c = ((xs[:, None] + dx_t[None, :]) % lat.nx) * P + rloc_t[None, :]
+        v = val_t.repeat(len(xs), 1)
+        if pot.depth != 0.0:
+            on = ((xs % pot.spacing[0]) < pot.dot[0]).to(torch.float64)
+            v[:, diag_t] += on[:, None] * vdot_t[None, :]
+        col[b0 * nnz_p : (b0 + len(xs)) * nnz_p] = c.reshape(-1)
+        val[b0 * nnz_p : (b0 + len(xs)) * nnz_p] = v.reshape(-1)
+    return row_ptr, col, val
+
+
 def gershgorin(row_ptr, col, val, row_begin: int = 0):
     """(lo, hi) of the union of Gershgorin discs of the given CSR rows."""
     n_loc = len(row_ptr) - 1
