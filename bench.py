@@ -32,7 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from workloads.ti_lattice import (CONFIGS, SEED, Lattice, chunk_order_yband, gershgorin, generate_csr,  # noqa: E402
-                                  scale_factors)
+                                  generate_csr_torch, scale_factors)
 
 S_D, S_I = 16, 4
 
@@ -189,9 +189,10 @@ def main():
     ap.add_argument("--M", type=int, default=None, help="default: the config's M (2000 for bar)")
     ap.add_argument("--R", type=int, default=None, help="default: the config's R (32 for bar)")
     ap.add_argument("--lattice", default="200,100,40", help="per-GPU x-slab nx,ny,nz (config bar)")
-    ap.add_argument("--config", default="bar", choices=["bar", "C1", "C2", "C3", "C4"],
+    ap.add_argument("--config", default="bar", choices=["bar", "C1", "C2", "C3", "C4", "C5"],
                     help="bar: (200N)x100x40 weak scaling (= C3 at N=1); C1..C4: the BASELINE.json lattices, "
-                         "global size fixed (strong scaling over N)")
+                         "global size fixed (strong scaling over N); C5: 1800x400x40 slab per GPU (~150 GB HBM), "
+                         "M=4000, generated and converted on the GPU (weak scaling)")
     ap.add_argument("--chunk-order", default="auto", choices=["auto", "none"],
                     help="auto: y-banded chunk order when the x-neighbour window exceeds ~32 MB (kpm_set_chunk_order)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -233,6 +234,10 @@ def main():
         px, ny, nz = (int(t) for t in args.lattice.split(","))
         nx = px * world
         scaling = "weak"
+    elif args.config == "C5":
+        px, ny, nz = 1800, 400, 40
+        nx = px * world
+        scaling = "weak"
     else:
         nx, ny, nz = CONFIGS[args.config]["lattice"]
         px = nx // world
@@ -241,14 +246,28 @@ def main():
         scaling = "strong"
     lat = Lattice(nx, ny, nz)
     x0, x1 = px * rank, px * (rank + 1)
-    rp, col, val = generate_csr(lat, x0, x1)
-    lo, hi = gershgorin(rp, col, val, row_begin=x0 * lat.rows_per_plane)
+    on_device = args.config == "C5"
+    if on_device:
+        # 1.5e9 nonzeros per GPU: generated on the GPU (workloads.generate_csr_torch) and passed
+        # to kpm_set_matrix as a device CSR.  Gershgorin discs depend only on a row's entries,
+        # which repeat in x with the potential's period (20 planes): a 21-plane host slab gives
+        # the exact global interval.
+        rps, cols_, vals_ = generate_csr(lat, 0, 21)
+        lo, hi = gershgorin(rps, cols_, vals_)
+        del rps, cols_, vals_
+        rp, col, val = generate_csr_torch(lat, x0, x1, device=f"cuda:{local}")
+        n_loc, nnz_loc = rp.numel() - 1, int(rp[-1].item())
+    else:
+        rp, col, val = generate_csr(lat, x0, x1)
+        lo, hi = gershgorin(rp, col, val, row_begin=x0 * lat.rows_per_plane)
+        n_loc, nnz_loc = len(rp) - 1, int(rp[-1])
     lo, hi = -allmax(-lo), allmax(hi)
     a, b = scale_factors(lo, hi)
     n, nnz = lat.n, lat.nnz_expected()
-    n_loc, nnz_loc = len(rp) - 1, int(rp[-1])
     if args.config == "bar":
         M, R = args.M or 2000, args.R or 32
+    elif args.config == "C5":
+        M, R = args.M or 4000, args.R or 32
     else:
         M, R = args.M or CONFIGS[args.config]["M"], args.R or CONFIGS[args.config]["R"]
     uid = None
@@ -267,7 +286,11 @@ def main():
         os.dup2(saved, 1)
         os.close(saved)
     row_begin = x0 * lat.rows_per_plane
-    ctx.set_matrix(rp, col, val, a, b, n_global=n, row_begin=row_begin)
+    ctx.set_matrix(rp, col, val, a, b, n_global=n, row_begin=row_begin,
+                   mem=kpm.KPM_MEM_DEVICE if on_device else kpm.KPM_MEM_HOST)
+    if on_device:  # the library keeps its own SELL copy; free the 37 GB CSR before the vectors
+        del rp, col, val
+        torch.cuda.empty_cache()
     band = None
     if args.chunk_order == "auto" and 2 * lat.rows_per_plane * min(R, 32) * 16 > 32e6 and lat.nz % 8 == 0:
         band = max(1, int(16e6 // (2 * 4 * nz * min(R, 32) * 16)))
@@ -281,6 +304,7 @@ def main():
 
     for _ in range(args.warmup):
         ctx.moments(M, R, SEED)
+    free_b, total_b = torch.cuda.mem_get_info(local)
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sweep_ms = []
@@ -315,7 +339,7 @@ def main():
                                 f"C3 TI lattice {nx}x{ny}x{nz} x 4 orbitals, M={M}, R={R}" if world == 1 else
                                 f"Bar TI lattice {nx}x{ny}x{nz} x 4 orbitals (C3 slab per GPU), M={M}, R={R}"),
                    "lattice": [nx, ny, nz], "N": n, "N_nz": nnz, "M": M, "R": R, "parallelism": f"x-slab dp{world}",
-                   "kernel_variant": ctx.last_kernel(), "chunk_order": f"y-band {band}" if band else "storage", "halo": os.environ.get("KPM_HALO", "fused") if world > 1 else None,
+                   "hbm_in_use_gb": round((total_b - free_b) / 1e9, 1), "kernel_variant": ctx.last_kernel(), "chunk_order": f"y-band {band}" if band else "storage", "halo": os.environ.get("KPM_HALO", "fused") if world > 1 else None,
                    "l2": ("inputs larger than L2 (V, W %.2f GB each per GPU; matrix %.2f GB)" if
                           (32 * R * n_loc + 20 * nnz_loc) > 126e6 else
                           "L2-resident working set (V, W %.2f GB each, matrix %.2f GB; no flush)") % (
@@ -342,7 +366,10 @@ def main():
                             "P_mem_gflops": hbm / (bs / alg_flops_per_sweep(n, nnz, r)), "kernel": ctx.last_kernel()}
         out["by_R"] = by_r
     # e2e: host CSR in, mu/eta out, through the C ABI, copies inside the timed region
-    if not args.no_e2e:
+    if not args.no_e2e and on_device:
+        out["e2e"] = None
+        out["e2e_note"] = "C5 slabs (37 GB CSR per GPU) are generated on the device; no host-input e2e"
+    elif not args.no_e2e:
         h2d = rp.nbytes + col.nbytes + val.nbytes
         d2h = M * 8 + R * M * 16
         barrier()
@@ -360,7 +387,7 @@ def main():
                       "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
                       "ms_per_step": te / args.steps,
                       "note": "kpm_set_matrix(host CSR: validation, SELL build, H2D) + kpm_moments (D2H mu, eta)"}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not on_device:
         gf, threads, sweeps, t = oracle_sample(rp, col, val, a, b, n, nnz)
         out["cpu_baseline"] = {"value": gf, "unit": "Gflop/s", "cores": threads, "kind": "oracle",
                                "sample": f"same lattice, 1 random vector, {sweeps} sweeps ({t:.1f} s)"}
