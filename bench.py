@@ -365,6 +365,27 @@ def main():
                             "hbm_gbs_alg": bs / (sw * 1e-3) / 1e9, "frac": bs / (sw * 1e-3) / 1e9 / hbm,
                             "P_mem_gflops": hbm / (bs / alg_flops_per_sweep(n, nnz, r)), "kernel": ctx.last_kernel()}
         out["by_R"] = by_r
+        # P*_LLC as the paper measures it: the same kernel on a down-sized lattice whose
+        # whole working set (matrix + V + W, ~80 MB at R = 32) stays in the 126 MB L2
+        small = Lattice(20, 24, 40)
+        rps, cs, vs = generate_csr(small)
+        with kpm.KpmContext(device=local, cuda_stream=stream.cuda_stream) as c2:
+            c2.set_matrix(rps, cs, vs, a, b)
+            c2.moments(200, 32, SEED, want_eta=False)
+            c2.moments(200, 32, SEED, want_eta=False)
+            sw = c2.last_timing()[1]
+        fl = alg_flops_per_sweep(small.n, int(rps[-1]), 32)
+        out["cache_resident"] = {"lattice": [20, 24, 40], "R": 32, "sweep_ms": sw, "gflops": fl / (sw * 1e-3) / 1e9,
+                                 "working_set_mb": round((32 * 32 * small.n + 20 * int(rps[-1])) / 1e6, 1),
+                                 "note": "P*_LLC of the paper's custom roofline; 1500 chunks under-fill 148 SMs "
+                                         "(P:741-743 notes the same for the K20m)"}
+        p_mem = hbm / bmin
+        p_llc = out["cache_resident"]["gflops"]
+        kern = out["roofline"]["kernel_gflops_per_gpu"]
+        out["custom_roofline"] = {"P_mem_gflops": p_mem, "P_llc_gflops": p_llc, "applicable_gflops": min(p_mem, p_llc),
+                                  "bound": "llc" if p_llc < p_mem else "hbm", "kernel_gflops": kern,
+                                  "frac": kern / min(p_mem, p_llc),
+                                  "model": "P* = min(P*_MEM, P*_LLC), Eq. (11) eq:roofline_custom, P:704"}
     # e2e: host CSR in, mu/eta out, through the C ABI, copies inside the timed region
     if not args.no_e2e and on_device:
         out["e2e"] = None

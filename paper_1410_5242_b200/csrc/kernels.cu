@@ -433,7 +433,7 @@ constexpr int kTileBudget = 232448 - 8192;  // minus static smem (reduction buff
 // Consumer warps per column part: one per row group of a chunk, at most 8 (so R < 8 uses
 // small CTAs: G = LPR row groups of 32/LPR rows each).
 template <int LPR>
-__host__ __device__ constexpr int tiled_ncwg() { return LPR < 8 ? LPR : 8; }
+__host__ __device__ constexpr int tiled_ncwg() { return LPR < 8 ? LPR : (LPR == 16 ? 16 : 8); }
 template <int LPR, int CS>
 __host__ __device__ constexpr int tiled_threads() { return 32 * (tiled_ncwg<LPR>() * CS + 1); }
 
@@ -693,7 +693,7 @@ const Entry kTable[] = {
     KPM_VARIANT(16, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT_WR(16, 8, 4, "tiled.lpr8.u4.wr"),
     KPM_VARIANT_CS(16, 8, 4, 2, "tiled.lpr8.u4.cs2"),
-    KPM_VARIANT(16, 16, 4, kTiled, "tiled.lpr16.u4"),
+    KPM_VARIANT(16, 16, 4, kTiled, "tiled.lpr16.u4.w16"),
     KPM_VARIANT(16, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(16, 8, 4, kDirect, "direct.lpr8.u4"),
     KPM_VARIANT(32, 8, 4, kTiled, "tiled.lpr8.u4"),

@@ -84,6 +84,11 @@ struct kpm_ctx {
   std::vector<int32_t*> dst_flag;   // per destination peer (parallel to dest_peers)
   std::vector<int> dest_peers, src_peers;
   int fused_rk = 0;
+  // CUDA graph of the single-rank sweep loop (cached per configuration)
+  bool use_graph = true;
+  cudaGraphExec_t graph_exec = nullptr;
+  std::vector<int64_t> graph_key;
+  int64_t matrix_gen = 0;           // bumped by every kpm_set_matrix / kpm_set_chunk_order
   double last_total_ms = 0.0, last_sweep_ms = 0.0;
   int last_n_sweeps = 0;
 };
@@ -176,6 +181,7 @@ extern "C" kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt) {
   ctx->variant_override = env_int("KPM_VARIANT", -1);
   ctx->grid_per_sm = std::max(0, env_int("KPM_GRID_PER_SM", 0));
   ctx->tile_stages = std::max(0, env_int("KPM_TILE_STAGES", 0));
+  ctx->use_graph = env_int("KPM_GRAPH", 1) != 0;
   *out = ctx;
   return KPM_OK;
 }
@@ -324,6 +330,7 @@ static kpm_status plan_exchange(kpm_ctx* ctx, const std::vector<int64_t>& halo, 
 // the plain range when no order is set); multi-rank -> edge and interior lists, each in order.
 static kpm_status apply_order(kpm_ctx* ctx) {
   const int64_t n = ctx->sell.n_chunks;
+  ++ctx->matrix_gen;
   std::vector<int64_t> ord = ctx->order_h;
   if (ord.empty()) {
     ord.resize(n);
@@ -573,6 +580,7 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
       ctx->epoch = 0;
     }
   }
+  ++ctx->matrix_gen;
   ctx->n_global = H->n_global;
   ctx->row_begin = H->row_begin;
   ctx->row_end = H->row_end;
@@ -848,10 +856,36 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   };
   // a2: init sweep, eta_0, eta_1
   if ((st = sweep(0)) != KPM_OK) return st;
-  // a3: main sweeps, eta_2m, eta_2m+1
+  // a3: main sweeps, eta_2m, eta_2m+1.  Single rank: the M/2-1 launches are captured once
+  // into a CUDA graph per configuration and replayed (launch overhead matters for small
+  // matrices, e.g. C1's 5-us sweeps); env KPM_GRAPH=0 launches them one by one.
   KPM_CUDA(cudaEventRecord(ctx->ev[1], str));
-  for (int m = 1; m < n_sweeps; ++m)
-    if ((st = sweep(m)) != KPM_OK) return st;
+  const bool use_graph = !multi && ctx->use_graph && n_sweeps > 2;
+  if (use_graph) {
+    const std::vector<int64_t> key = {Rk, variant, grid, n_sweeps, (int64_t)ctx->X0, (int64_t)ctx->X1,
+                                      (int64_t)ctx->partials, (int64_t)sa.chunk_list, (int64_t)sa.rec,
+                                      (int64_t)s.val, (int64_t)(ctx->a * 1e15), (int64_t)(ctx->b * 1e15),
+                                      ctx->matrix_gen, tl.stages};
+    if (!ctx->graph_exec || key != ctx->graph_key) {
+      if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+      ctx->graph_exec = nullptr;
+      cudaGraph_t g;
+      KPM_CUDA(cudaStreamBeginCapture(str, cudaStreamCaptureModeThreadLocal));
+      for (int m = 1; m < n_sweeps; ++m)
+        if ((st = sweep(m)) != KPM_OK) {
+          cudaStreamEndCapture(str, &g);
+          return st;
+        }
+      KPM_CUDA(cudaStreamEndCapture(str, &g));
+      KPM_CUDA(cudaGraphInstantiate(&ctx->graph_exec, g, 0));
+      KPM_CUDA(cudaGraphDestroy(g));
+      ctx->graph_key = key;
+    }
+    KPM_CUDA(cudaGraphLaunch(ctx->graph_exec, str));
+  } else {
+    for (int m = 1; m < n_sweeps; ++m)
+      if ((st = sweep(m)) != KPM_OK) return st;
+  }
   KPM_CUDA(cudaEventRecord(ctx->ev[2], str));
   // a4: deterministic grid reduction of all sweeps' partials
   KPM_CUDA(launch_eta_finalize(ctx->partials, n_sweeps, Rk, grid * parts, ctx->eta_even, ctx->eta_odd, str));

@@ -282,3 +282,34 @@ def test_device_build_errors(pkg):
             ctx.set_matrix(torch.as_tensor(rp, device="cuda"), bad, torch.as_tensor(val, device="cuda"), a, b,
                            n_global=lat.n, mem=pkg.KPM_MEM_DEVICE)
         assert ei.value.status == pkg.KPM_ERANGE
+
+
+@pytest.mark.parametrize("R", [1, 8, 32])
+def test_irregular_matrix_fallback(pkg, R):
+    """A random Hermitian matrix with empty rows, wide rows (up to ~200 entries) and scattered
+    columns: no tile plan fits (too many runs / rows per chunk), so the default selection falls
+    back to the direct feed -- still oracle-exact."""
+    rng = np.random.default_rng(11)
+    n = 3000
+    rows, cols = [], []
+    for i in range(n):
+        k = 0 if i % 97 == 0 else int(rng.integers(1, 200 if i % 13 == 0 else 12))
+        rows += [i] * k
+        cols += rng.integers(0, n, k).tolist()
+    rows, cols = np.array(rows), np.array(cols)
+    keep = (rows % 97 != 0) & (cols % 97 != 0)  # rows (and columns) 0, 97, ... stay empty
+    rows, cols = rows[keep], cols[keep]
+    z = rng.normal(size=len(rows)) + 1j * rng.normal(size=len(rows))
+    import scipy.sparse as sp
+
+    h = sp.coo_matrix((z, (rows, cols)), shape=(n, n)).tocsr()
+    h = (h + h.conj().T).tocsr()
+    h.sort_indices()
+    rp, col, val = h.indptr.astype(np.int64), h.indices.astype(np.int64), h.data.astype(np.complex128)
+    a, b = scale_factors(*gershgorin(rp, col, val))
+    M = 40
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments(M, R, SEED)
+        assert ctx.last_kernel().startswith("direct")
+    check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, M, R, SEED))
