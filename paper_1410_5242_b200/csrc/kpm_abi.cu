@@ -703,7 +703,22 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     if ((st = allgather_i64(ctx, {ctx->fused_ready && ctx->fused_rk == Rk ? 1 : 0}, all)) != KPM_OK) return st;
     bool ready = true;
     for (int64_t v : all) ready = ready && v == 1;
-    if (!ready && (st = setup_fused(ctx, Rk)) != KPM_OK) return st;
+    if (!ready) {
+      // IPC mapping can fail (no P2P between the GPUs, restricted containers): then every rank
+      // falls back to the NCCL exchange together
+      const kpm_status fst = setup_fused(ctx, Rk);
+      if (fst != KPM_OK) {
+        cudaGetLastError();
+        ctx->sticky = false;
+        ctx->fused_ready = false;
+      }
+      std::vector<int64_t> oks;
+      if ((st = allgather_i64(ctx, {fst == KPM_OK ? 1 : 0}, oks)) != KPM_OK) return st;
+      for (int64_t v : oks)
+        if (v != 1) ctx->fused = false;
+      if (!ctx->fused) fprintf(stderr, "kpm: fused NVLink halo exchange unavailable (%s); using NCCL P2P\n",
+                               fst == KPM_OK ? "another rank failed" : ctx->err.c_str());
+    }
   }
 
   const int lg = __builtin_ctz(Rk);
