@@ -118,6 +118,16 @@ kpm_status kpm_moments(kpm_ctx* ctx, int M, int R, uint64_t seed, double* mu, do
  * by eta_0).  KPM_EZERONORM if a column has eta_0 == 0 (mu/eta still written). */
 kpm_status kpm_moments_v0(kpm_ctx* ctx, int M, int R, const double* v0, double* mu, double* eta);
 
+/* The paper's three optimisation stages (Figs. 3-5), same outputs as
+ * kpm_moments, for measuring what fusion and blocking buy:
+ *   KPM_STAGE_NAIVE      Fig. 3: per column, separate spmv, axpy, scal, axpy, nrm2, dot kernels
+ *                        (single rank only)
+ *   KPM_STAGE_AUG_SPMV   Fig. 4: per column, the fused sweep with block width 1 ("throughput
+ *                        mode" of Table III when the columns are independent runs)
+ *   KPM_STAGE_AUG_SPMMV  Fig. 5: = kpm_moments (all columns in one sweep). */
+enum { KPM_STAGE_NAIVE = 0, KPM_STAGE_AUG_SPMV = 1, KPM_STAGE_AUG_SPMMV = 2 };
+kpm_status kpm_moments_stage(kpm_ctx* ctx, int stage, int M, int R, uint64_t seed, double* mu, double* eta);
+
 /* Device time of the last kpm_moments* call, measured with CUDA events on the context's
  * stream: total_ms = start-vector init .. last eta reduction; sweep_ms = average duration
  * of one main aug_spmmv sweep (the hot kernel); n_sweeps = main sweeps timed. */

@@ -21,7 +21,7 @@ STATUS_NAMES = ["KPM_OK", "KPM_EINVAL", "KPM_ESTATE", "KPM_ERANGE", "KPM_ENOMEM"
 
 # exported symbols declared in include/kpm.h
 ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_dos", "kpm_export_sell", "kpm_get_sell_info", "kpm_get_unique_id",
-               "kpm_last_error", "kpm_last_kernel", "kpm_last_timing", "kpm_moments", "kpm_moments_v0",
+               "kpm_last_error", "kpm_last_kernel", "kpm_last_timing", "kpm_moments", "kpm_moments_stage", "kpm_moments_v0",
                "kpm_plan_recv", "kpm_plan_send", "kpm_set_chunk_order", "kpm_set_matrix"]
 
 
@@ -65,6 +65,7 @@ def load_library():
     lib.kpm_set_matrix.argtypes = [P, ctypes.POINTER(kpm_csr), dbl, dbl]
     lib.kpm_moments.argtypes = [P, i32, i32, u64, P, P]
     lib.kpm_moments_v0.argtypes = [P, i32, i32, P, P, P]
+    lib.kpm_moments_stage.argtypes = [P, i32, i32, i32, u64, P, P]
     lib.kpm_last_timing.argtypes = [P, P, P, P]
     lib.kpm_get_sell_info.argtypes = [P, ctypes.POINTER(kpm_sell_info)]
     lib.kpm_export_sell.argtypes = [P, P, P, P, P, P]
@@ -206,6 +207,14 @@ class KpmContext:
         eta = np.zeros((R, M), dtype=np.complex128) if want_eta else None
         allow = (KPM_WDIVERGED,) if allow_warning else ()
         self._check(self.lib.kpm_moments(self.h, M, R, seed, _ptr(mu), _ptr(eta)), allow)
+        return mu, eta
+
+    def moments_stage(self, stage, M, R, seed, want_eta=True):
+        """kpm_moments_stage: 'naive' (Fig. 3), 'aug_spmv' (Fig. 4) or 'aug_spmmv' (Fig. 5)."""
+        code = {"naive": 0, "aug_spmv": 1, "aug_spmmv": 2}[stage]
+        mu = np.zeros(M)
+        eta = np.zeros((R, M), dtype=np.complex128) if want_eta else None
+        self._check(self.lib.kpm_moments_stage(self.h, code, M, R, seed, _ptr(mu), _ptr(eta)), (KPM_WDIVERGED,))
         return mu, eta
 
     def moments_v0(self, M, v0, allow=(KPM_WDIVERGED,)):

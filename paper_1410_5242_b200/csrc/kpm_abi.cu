@@ -57,6 +57,8 @@ struct kpm_ctx {
   double2* h_eta = nullptr;  // pinned staging, 2*eta_cap
   double2* v0_dev = nullptr;
   size_t v0_cap = 0;
+  double2* u_naive = nullptr;  // naive stage's u vector
+  size_t u_cap = 0;
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
@@ -199,6 +201,7 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   cudaFree(ctx->eta_even);
   cudaFree(ctx->eta_odd);
   cudaFree(ctx->v0_dev);
+  cudaFree(ctx->u_naive);
   if (ctx->h_eta) cudaFreeHost(ctx->h_eta);
   for (int i = 0; i < 4; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
@@ -934,6 +937,33 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   return KPM_OK;
 }
 
+// a6: eta -> mu (doubling identities, stochastic trace)
+static kpm_status finish_mu(kpm_ctx* ctx, int M, int R, const std::vector<double2>& eta_all, bool explicit_v0,
+                            double* mu, double* eta) {
+  bool zero_norm = false;
+  std::vector<double> acc(M, 0.0);
+  std::vector<double2> m(M);
+  for (int r = 0; r < R; ++r) {
+    const double2* e = eta_all.data() + (size_t)r * M;
+    if (e[0].x == 0.0) zero_norm = true;
+    m[0] = e[0];
+    m[1] = e[1];
+    for (int k = 1; 2 * k < M; ++k) {
+      m[2 * k] = make_double2(2.0 * e[2 * k].x - m[0].x, 2.0 * e[2 * k].y - m[0].y);
+      m[2 * k + 1] = make_double2(2.0 * e[2 * k + 1].x - m[1].x, 2.0 * e[2 * k + 1].y - m[1].y);
+    }
+    for (int n = 0; n < M; ++n) acc[n] += m[n].x;
+  }
+  bool diverged = false;
+  for (int n = 0; n < M; ++n) mu[n] = acc[n] / (double)R;
+  for (int n = 1; n < M; ++n)
+    if (!(std::fabs(mu[n]) <= std::fabs(mu[0]) * (1.0 + 1e-8))) diverged = true;
+  if (eta) std::memcpy(eta, eta_all.data(), sizeof(double2) * (size_t)R * M);
+  if (explicit_v0 && zero_norm) return fail(ctx, KPM_EZERONORM, "a start column has eta_0 = 0");
+  if (diverged) return fail(ctx, KPM_WDIVERGED, "|mu_n| > mu_0: a, b do not map the spectrum into [-1, 1]");
+  return KPM_OK;
+}
+
 static kpm_status moments_common(kpm_ctx* ctx, int M, int R, uint64_t seed, const double* v0, double* mu,
                                  double* eta) {
   if (!ctx) return KPM_EINVAL;
@@ -962,33 +992,100 @@ static kpm_status moments_common(kpm_ctx* ctx, int M, int R, uint64_t seed, cons
                               c0 + kMaxBlockWidth >= R);
     if (st != KPM_OK) return st;
   }
-  // a6: eta -> mu (doubling identities, stochastic trace)
-  bool zero_norm = false;
-  std::vector<double> acc(M, 0.0);
-  std::vector<double2> m(M);
-  for (int r = 0; r < R; ++r) {
-    const double2* e = eta_all.data() + (size_t)r * M;
-    if (e[0].x == 0.0) zero_norm = true;
-    m[0] = e[0];
-    m[1] = e[1];
-    for (int k = 1; 2 * k < M; ++k) {
-      m[2 * k] = make_double2(2.0 * e[2 * k].x - m[0].x, 2.0 * e[2 * k].y - m[0].y);
-      m[2 * k + 1] = make_double2(2.0 * e[2 * k + 1].x - m[1].x, 2.0 * e[2 * k + 1].y - m[1].y);
+  return finish_mu(ctx, M, R, eta_all, v0 != nullptr, mu, eta);
+}
+
+// Naive stage-0 KPM of Fig. 3 for one column (naive.cu), same outputs as run_block.
+static kpm_status naive_column(kpm_ctx* ctx, int M, int64_t col_begin, uint64_t seed, double2* eta_cols, bool first,
+                               bool last) {
+  const int n_sweeps = M / 2;
+  const DevSell& s = ctx->sell;
+  const int64_t n_rows_total = s.n_pad + s.n_halo;
+  kpm_status st;
+  size_t xcap = ctx->x_cap;
+  if ((st = ensure(ctx, (void**)&ctx->X0, &xcap, (size_t)n_rows_total, sizeof(double2))) != KPM_OK) return st;
+  xcap = ctx->x_cap;
+  if ((st = ensure(ctx, (void**)&ctx->X1, &xcap, (size_t)n_rows_total, sizeof(double2))) != KPM_OK) return st;
+  if (xcap != ctx->x_cap) ctx->fused_ready = false;
+  ctx->x_cap = xcap;
+  if ((st = ensure(ctx, (void**)&ctx->u_naive, &ctx->u_cap, (size_t)s.n_pad, sizeof(double2))) != KPM_OK) return st;
+  const int g = naive_grid();
+  if ((st = ensure(ctx, (void**)&ctx->partials, &ctx->partials_cap, (size_t)3 * g * n_sweeps, sizeof(double))) != KPM_OK)
+    return st;
+  size_t ecap = ctx->eta_cap;
+  if ((st = ensure(ctx, (void**)&ctx->eta_even, &ecap, (size_t)n_sweeps * kMaxBlockWidth, sizeof(double2))) != KPM_OK)
+    return st;
+  ecap = ctx->eta_cap;
+  if ((st = ensure(ctx, (void**)&ctx->eta_odd, &ecap, (size_t)n_sweeps * kMaxBlockWidth, sizeof(double2))) != KPM_OK)
+    return st;
+  if (ecap > ctx->eta_cap || !ctx->h_eta) {
+    if (ctx->h_eta) cudaFreeHost(ctx->h_eta);
+    ctx->h_eta = nullptr;
+    if (cudaMallocHost((void**)&ctx->h_eta, sizeof(double2) * 2 * ecap) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, KPM_ENOMEM, "pinned host allocation failed");
     }
-    for (int n = 0; n < M; ++n) acc[n] += m[n].x;
   }
-  bool diverged = false;
-  for (int n = 0; n < M; ++n) mu[n] = acc[n] / (double)R;
-  for (int n = 1; n < M; ++n)
-    if (!(std::fabs(mu[n]) <= std::fabs(mu[0]) * (1.0 + 1e-8))) diverged = true;
-  if (eta) std::memcpy(eta, eta_all.data(), sizeof(double2) * (size_t)R * M);
-  if (v0 && zero_norm) return fail(ctx, KPM_EZERONORM, "a start column has eta_0 = 0");
-  if (diverged) return fail(ctx, KPM_WDIVERGED, "|mu_n| > mu_0: a, b do not map the spectrum into [-1, 1]");
+  ctx->eta_cap = ecap;
+  cudaStream_t str = ctx->stream;
+  if (first) KPM_CUDA(cudaEventRecord(ctx->ev[0], str));
+  KPM_CUDA(launch_z4_init(ctx->X0, ctx->X1, s.perm, s.n_loc, s.n_pad, ctx->halo_rows, n_rows_total, 1, ctx->row_begin,
+                          col_begin, 1, seed, str));
+  KPM_CUDA(naive_sweep(s, ctx->X0, ctx->X1, ctx->u_naive, ctx->a, ctx->b, true, ctx->partials, str));
+  KPM_CUDA(cudaEventRecord(ctx->ev[1], str));
+  for (int m = 1; m < n_sweeps; ++m) {  // swap(|w>, |v>) is the pointer swap
+    const double2* v = (m & 1) ? ctx->X1 : ctx->X0;
+    double2* w = (m & 1) ? ctx->X0 : ctx->X1;
+    KPM_CUDA(naive_sweep(s, v, w, ctx->u_naive, ctx->a, ctx->b, false, ctx->partials + (size_t)3 * g * m, str));
+  }
+  KPM_CUDA(cudaEventRecord(ctx->ev[2], str));
+  KPM_CUDA(launch_eta_finalize(ctx->partials, n_sweeps, 1, g, ctx->eta_even, ctx->eta_odd, str));
+  KPM_CUDA(cudaMemcpyAsync(ctx->h_eta, ctx->eta_even, sizeof(double2) * n_sweeps, cudaMemcpyDeviceToHost, str));
+  KPM_CUDA(cudaMemcpyAsync(ctx->h_eta + ctx->eta_cap, ctx->eta_odd, sizeof(double2) * n_sweeps, cudaMemcpyDeviceToHost,
+                           str));
+  if (last) KPM_CUDA(cudaEventRecord(ctx->ev[3], str));
+  KPM_CUDA(cudaStreamSynchronize(str));
+  for (int m = 0; m < n_sweeps; ++m) {
+    eta_cols[2 * m] = ctx->h_eta[m];
+    eta_cols[2 * m + 1] = ctx->h_eta[ctx->eta_cap + m];
+  }
+  float ms = 0.f;
+  if (n_sweeps > 1) {
+    KPM_CUDA(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]));
+    ctx->last_sweep_ms = ms / (n_sweeps - 1);
+    ctx->last_n_sweeps = n_sweeps - 1;
+  }
+  if (last) {
+    KPM_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]));
+    ctx->last_total_ms = ms;
+  }
   return KPM_OK;
 }
 
 extern "C" kpm_status kpm_moments(kpm_ctx* ctx, int M, int R, uint64_t seed, double* mu, double* eta) {
   return moments_common(ctx, M, R, seed, nullptr, mu, eta);
+}
+
+extern "C" kpm_status kpm_moments_stage(kpm_ctx* ctx, int stage, int M, int R, uint64_t seed, double* mu,
+                                        double* eta) {
+  if (stage == KPM_STAGE_AUG_SPMMV) return moments_common(ctx, M, R, seed, nullptr, mu, eta);
+  if (!ctx) return KPM_EINVAL;
+  if (stage != KPM_STAGE_NAIVE && stage != KPM_STAGE_AUG_SPMV) return fail(ctx, KPM_EINVAL, "unknown stage");
+  if (ctx->sticky) return fail(ctx, KPM_ESTATE, "context has a sticky CUDA/NCCL error: " + ctx->err);
+  if (!ctx->have_matrix) return fail(ctx, KPM_ESTATE, "kpm_set_matrix has not been called");
+  if (M < 2 || (M % 2) != 0) return fail(ctx, KPM_EINVAL, "M must be even and >= 2");
+  if (R < 1 || !mu) return fail(ctx, KPM_EINVAL, "R must be >= 1 and mu non-NULL");
+  if (stage == KPM_STAGE_NAIVE && ctx->opt.nranks > 1) return fail(ctx, KPM_EINVAL, "the naive stage is single-rank");
+  KPM_CUDA(cudaSetDevice(ctx->opt.device));
+  std::vector<double2> eta_all((size_t)R * M);
+  for (int r = 0; r < R; ++r) {  // outer loop over the random vectors (Figs. 3, 4: P:266)
+    const kpm_status st = stage == KPM_STAGE_NAIVE
+                              ? naive_column(ctx, M, r, seed, eta_all.data() + (size_t)r * M, r == 0, r == R - 1)
+                              : run_block(ctx, M, 1, r, seed, nullptr, eta_all.data() + (size_t)r * M, r == 0, r == R - 1);
+    if (st != KPM_OK) return st;
+  }
+  if (stage == KPM_STAGE_NAIVE) ctx->last_variant = "naive.blas1";
+  return finish_mu(ctx, M, R, eta_all, false, mu, eta);
 }
 
 extern "C" kpm_status kpm_moments_v0(kpm_ctx* ctx, int M, int R, const double* v0, double* mu, double* eta) {

@@ -96,6 +96,11 @@ cudaError_t launch_aug_spmmv(int R, int variant, bool init, const SweepArgs& a, 
 cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int width, double2* eta_even,
                                 double2* eta_odd, cudaStream_t s);
 
+// Naive stage-0 sweep of one column (naive.cu): separate spmv/axpy/scal/axpy/nrm2/dot kernels.
+int naive_grid();
+cudaError_t naive_sweep(const DevSell& s, const double2* v, double2* w, double2* u, double a, double b, bool init,
+                        double* part, cudaStream_t st);
+
 // Device-side setup (sell_device.cu): CSR on the device -> SELL-32 (sigma = 1) + tile plan.
 struct DeviceBuild {
   std::vector<int64_t> halo;     // global ids of the halo slots (host copy)

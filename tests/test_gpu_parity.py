@@ -313,3 +313,15 @@ def test_irregular_matrix_fallback(pkg, R):
         mu, eta = ctx.moments(M, R, SEED)
         assert ctx.last_kernel().startswith("direct")
     check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, M, R, SEED))
+
+
+@pytest.mark.parametrize("stage", ["naive", "aug_spmv", "aug_spmmv"])
+def test_optimisation_stages(pkg, stage):
+    """The three stages of Figs. 3-5 give the same moments (P:89-90 'the algorithm itself is
+    untouched'), each against the oracle."""
+    lat, rp, col, val, a, b = problem((6, 5, 8))
+    M, R = 40, 5
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments_stage(stage, M, R, SEED)
+    check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, M, R, SEED, mode=oracle.CHAINED))
