@@ -140,9 +140,10 @@ def oracle_sample(rp, col, val, a, b, n, nnz, target_s=15.0, max_sweeps=400):
     import oracle
 
     threads = host_cores()
+    oracle.kpm_eta(rp, col, val, a, b, 4, 1, SEED, threads=threads)  # warm-up (threads, page faults)
     t0 = time.perf_counter()
-    oracle.kpm_eta(rp, col, val, a, b, 4, 1, SEED, threads=threads)  # 2 sweeps, calibrate
-    t_cal = (time.perf_counter() - t0) / 2
+    oracle.kpm_eta(rp, col, val, a, b, 8, 1, SEED, threads=threads)  # 4 sweeps, calibrate
+    t_cal = (time.perf_counter() - t0) / 4
     sweeps = int(max(2, min(max_sweeps, target_s / max(t_cal, 1e-6))))
     t0 = time.perf_counter()
     oracle.kpm_eta(rp, col, val, a, b, 2 * sweeps, 1, SEED, threads=threads)
