@@ -439,13 +439,7 @@ __host__ __device__ constexpr int tiled_threads() { return 32 * (tiled_ncwg<LPR>
 
 // WS: the old W rows travel in the tile (TMA) or, WS = false, straight into registers (LDG,
 // streaming) -- a smaller stage, so more CTAs fit per SM.
-// DD (R = 32, LPR = 32): register reuse of gathered rows.  A warp owns 4 consecutive rows of the
-// chunk, lane = block column; at every entry j the warp loads each *distinct* tile row among the
-// 4 rows' columns once (a warp-uniform comparison of the 4 indices) and applies it to every row
-// that references it.  For the 4 orbitals of a lattice site the hopping blocks pair the rows
-// (2 distinct neighbour rows per entry), so the shared-memory reads of V drop to ~0.54 per
-// nonzero.  Correct for any matrix; the saving is structural.
-template <int R, int LPR, int U, int CS, bool WS, bool INIT, bool DD = false>
+template <int R, int LPR, int U, int CS, bool WS, bool INIT>
 __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(const SweepArgs a) {
   using Cf = Cfg<R, LPR, U>;
   constexpr int RW = Cf::RW, G = kC / RW;
@@ -532,52 +526,6 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
       mbar_wait(smem_u32(&full[s]), (uint32_t)((k / tl.stages) & 1));
       const int L = tile_len[s];
       const int64_t c = tile_chunk[s];
-      if constexpr (DD) {
-        static_assert(R == 32 && LPR == 32 && CS == 1 && WS, "register-reuse consumer: R = 32 lanes = columns");
-        const int kr0 = 4 * g0;  // rows kr0 .. kr0+3 of the chunk, lane = column
-        const int64_t p0 = c * kC + kr0;
-        double2 u0 = make_double2(0.0, 0.0), u1 = u0, u2 = u0, u3 = u0;
-        const double2* sVt = sV + lane;
-        for (int j = 0; j < L; ++j) {
-          const uint2 l4 = *reinterpret_cast<const uint2*>(slc + j * kC + kr0);
-          const int i0 = (int)(l4.x & 0xffffu), i1 = (int)(l4.x >> 16), i2 = (int)(l4.y & 0xffffu),
-                    i3 = (int)(l4.y >> 16);
-          const double2* hv = sval + j * kC + kr0;
-          const double2 h0 = hv[0], h1 = hv[1], h2 = hv[2], h3 = hv[3];
-          const double2 x0 = sVt[i0 * R];
-          double2 x1, x2, x3;
-          if (i1 == i0) x1 = x0; else x1 = sVt[i1 * R];
-          if (i2 == i0) x2 = x0; else if (i2 == i1) x2 = x1; else x2 = sVt[i2 * R];
-          if (i3 == i0) x3 = x0; else if (i3 == i1) x3 = x1; else if (i3 == i2) x3 = x2; else x3 = sVt[i3 * R];
-          cmac(u0, h0, x0);
-          cmac(u1, h1, x1);
-          cmac(u2, h2, x2);
-          cmac(u3, h3, x3);
-        }
-        const double2 us[4] = {u0, u1, u2, u3};
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          const int64_t p = p0 + qq;
-          if (p < a.n_loc) {
-            const double2 vi = sV[(kr0 + qq) * R + lane];
-            double2 uu = us[qq];
-            uu.x = fma(-a.b, vi.x, uu.x);
-            uu.y = fma(-a.b, vi.y, uu.y);
-            double2 w;
-            if (INIT) {
-              w = make_double2(a.scale * uu.x, a.scale * uu.y);
-            } else {
-              const double2 wo = sW[(kr0 + qq) * R + lane];
-              w = make_double2(fma(a.scale, uu.x, -wo.x), fma(a.scale, uu.y, -wo.y));
-            }
-            st_stream(a.W + p * R + lane, w, pol);
-            store_peers<R>(a, p, lane, w);
-            d.ee[0] = fma(vi.x, vi.x, fma(vi.y, vi.y, d.ee[0]));
-            d.eor[0] = fma(w.x, vi.x, fma(w.y, vi.y, d.eor[0]));
-            d.eoi[0] = fma(w.x, vi.y, fma(-w.y, vi.x, d.eoi[0]));
-          }
-        }
-      } else
       for (int gq = g0; gq < G; gq += NCWG) {
         const int kr = gq * RW + q;
         const int64_t p = c * kC + kr;
@@ -674,7 +622,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
 
 enum Feed { kDirect = 0, kStaged = 1, kTiled = 2 };
 
-template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true, bool DD = false>
+template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true>
 struct Variant {
   static cudaError_t launch(bool init, const SweepArgs& a, int grid, cudaStream_t s) {
     if constexpr (FEED == kStaged) {
@@ -684,12 +632,12 @@ struct Variant {
         aug_spmmv_staged<R, LPR, U, false><<<grid, kThreads, kStagedSmem, s>>>(a);
     } else if constexpr (FEED == kTiled) {
       const int smem = a.tl.stages * a.tl.stage_bytes;
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, true, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, false, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (init)
-        aug_spmmv_tiled<R, LPR, U, CS, WS, true, DD><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
+        aug_spmmv_tiled<R, LPR, U, CS, WS, true><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
       else
-        aug_spmmv_tiled<R, LPR, U, CS, WS, false, DD><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
+        aug_spmmv_tiled<R, LPR, U, CS, WS, false><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
     } else {
       if (init)
         aug_spmmv_direct<R, LPR, U, true><<<grid, kThreads, 0, s>>>(a);
@@ -703,8 +651,8 @@ struct Variant {
     if constexpr (FEED == kStaged) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_staged<R, LPR, U, false>, kThreads, kStagedSmem);
     } else if constexpr (FEED == kTiled) {
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, false, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_tiled<R, LPR, U, CS, WS, false, DD>, tiled_threads<LPR, CS>(),
+      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_tiled<R, LPR, U, CS, WS, false>, tiled_threads<LPR, CS>(),
                                                     dyn_smem);
     } else {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_direct<R, LPR, U, false>, kThreads, 0);
@@ -726,8 +674,6 @@ struct Entry {
 #define KPM_VARIANT(R, LPR, U, F, NAME) {R, NAME, F, true, Variant<R, LPR, U, F>::launch, Variant<R, LPR, U, F>::occupancy}
 #define KPM_VARIANT_CS(R, LPR, U, CS, NAME) \
   {R, NAME, kTiled, true, Variant<R, LPR, U, kTiled, CS>::launch, Variant<R, LPR, U, kTiled, CS>::occupancy}
-#define KPM_VARIANT_DD(R, NAME) \
-  {R, NAME, kTiled, true, Variant<R, 32, 1, kTiled, 1, true, true>::launch, Variant<R, 32, 1, kTiled, 1, true, true>::occupancy}
 #define KPM_VARIANT_WR(R, LPR, U, NAME) \
   {R, NAME, kTiled, false, Variant<R, LPR, U, kTiled, 1, false>::launch, Variant<R, LPR, U, kTiled, 1, false>::occupancy}
 // First entry of each width is the default (chosen from the B200 measurements in DESIGN.md).
@@ -751,7 +697,6 @@ const Entry kTable[] = {
     KPM_VARIANT(16, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(16, 8, 4, kDirect, "direct.lpr8.u4"),
     KPM_VARIANT(32, 8, 4, kTiled, "tiled.lpr8.u4"),
-    KPM_VARIANT_DD(32, "tiled.dd"),
     KPM_VARIANT_WR(32, 8, 4, "tiled.lpr8.u4.wr"),
     KPM_VARIANT_CS(32, 8, 4, 2, "tiled.lpr8.u4.cs2"),
     KPM_VARIANT(32, 8, 2, kTiled, "tiled.lpr8.u2"),
