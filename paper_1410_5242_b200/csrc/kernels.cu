@@ -516,6 +516,11 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
     const int q = lane / LPR;
     const int g0 = warp % NCWG, part = warp / NCWG;
     const int t = lane - q * LPR + part * CPL * LPR;  // first block column of this lane
+    // Bank-conflict swizzle for LPR < 8: the 8 lanes of one shared-memory phase span 8/LPR
+    // rows whose LPR*16-byte segments would sit on the same banks; row q visits its column
+    // blocks in the order cc ^ (q mod 8/LPR), so the rows of a phase cover one 128-B window.
+    constexpr int SWR = (LPR < 8 && CPL * LPR >= 8) ? 8 / LPR : 1;
+    const int sw = q % SWR;
     for (int64_t k = 0; k < my_tiles; ++k) {
       const int s = (int)(k % tl.stages);
       const unsigned char* st = tsm + (size_t)s * tl.stage_bytes;
@@ -532,7 +537,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
         double2 wreg[CPL];
         if (!WS && !INIT && p < a.n_loc) {  // old W straight from HBM, lands under the gathers
 #pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) wreg[cc] = ld_stream(a.W + p * R + cc * LPR + t, pol);
+          for (int cc = 0; cc < CPL; ++cc) wreg[cc] = ld_stream(a.W + p * R + (cc ^ sw) * LPR + t, pol);
         }
         double2 u[CPL];
 #pragma unroll
@@ -553,7 +558,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
 #pragma unroll
           for (int uu = 0; uu < U; ++uu)
 #pragma unroll
-            for (int cc = 0; cc < CPL; ++cc) x[uu][cc] = sVt[li[uu] + cc * LPR];
+            for (int cc = 0; cc < CPL; ++cc) x[uu][cc] = sVt[li[uu] + (cc ^ sw) * LPR];
 #pragma unroll
           for (int uu = 0; uu < U; ++uu)
 #pragma unroll
@@ -563,12 +568,12 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
           const double2 h = sv[j * kC];
           const int li = sl[j * kC] * R;
 #pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h, sVt[li + cc * LPR]);
+          for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h, sVt[li + (cc ^ sw) * LPR]);
         }
         if (p < a.n_loc) {
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) {
-            const int col = cc * LPR + t;
+            const int col = (cc ^ sw) * LPR + t;
             const double2 vi = sV[kr * R + col];
             double2 uu = u[cc];
             uu.x = fma(-a.b, vi.x, uu.x);
@@ -590,6 +595,19 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&empty[s]));  // stage s released by this warp
+    }
+    // undo the swizzle so that accumulator cc holds column block cc on every lane
+    if (SWR > 1) {
+      Dots<CPL> e = d;
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc)
+#pragma unroll
+        for (int k2 = 0; k2 < CPL; ++k2)
+          if ((k2 ^ sw) == cc) {
+            d.ee[cc] = e.ee[k2];
+            d.eor[cc] = e.eor[k2];
+            d.eoi[cc] = e.eoi[k2];
+          }
     }
     // warp-level part of the dot-product reduction
 #pragma unroll
@@ -687,10 +705,12 @@ const Entry kTable[] = {
     KPM_VARIANT(4, 4, 4, kTiled, "tiled.lpr4.u4"),
     KPM_VARIANT(4, 4, 4, kDirect, "direct.lpr4.u4"),
     KPM_VARIANT(4, 4, 8, kDirect, "direct.lpr4.u8"),
+    KPM_VARIANT(8, 4, 4, kTiled, "tiled.lpr4.u4"),
     KPM_VARIANT(8, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kDirect, "direct.lpr8.u4"),
     KPM_VARIANT(16, 8, 4, kTiled, "tiled.lpr8.u4"),
+    KPM_VARIANT(16, 4, 2, kTiled, "tiled.lpr4.u2"),
     KPM_VARIANT_WR(16, 8, 4, "tiled.lpr8.u4.wr"),
     KPM_VARIANT_CS(16, 8, 4, 2, "tiled.lpr8.u4.cs2"),
     KPM_VARIANT(16, 16, 4, kTiled, "tiled.lpr16.u4.w16"),

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "every_kernel" 2>&1 | tail -2
+echo short; timeout 300 python scripts/variant_sweep.py --R 8,16,32 2>&1 | grep 'tiled.lpr[48]\.' | cut -c1-140
+echo sustained; timeout 600 python scripts/variant_sweep.py --R 8,16,32 --M 200 --warm-seconds 4 2>&1 | grep 'tiled.lpr[48]\.' | cut -c1-140
