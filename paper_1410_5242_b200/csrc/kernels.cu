@@ -688,10 +688,14 @@ struct Entry {
   bool wstage;
   LaunchFn launch;
   OccFn occ;
+  int stages = 0;  // tiled feed: preferred ring depth (0 = plan_tiles default)
 };
 #define KPM_VARIANT(R, LPR, U, F, NAME) {R, NAME, F, true, Variant<R, LPR, U, F>::launch, Variant<R, LPR, U, F>::occupancy}
 #define KPM_VARIANT_CS(R, LPR, U, CS, NAME) \
   {R, NAME, kTiled, true, Variant<R, LPR, U, kTiled, CS>::launch, Variant<R, LPR, U, kTiled, CS>::occupancy}
+#define KPM_VARIANT_WR_S(R, LPR, U, S, NAME)                                                             \
+  {R, NAME, kTiled, false, Variant<R, LPR, U, kTiled, 1, false>::launch, Variant<R, LPR, U, kTiled, 1, false>::occupancy, \
+   S}
 #define KPM_VARIANT_WR(R, LPR, U, NAME) \
   {R, NAME, kTiled, false, Variant<R, LPR, U, kTiled, 1, false>::launch, Variant<R, LPR, U, kTiled, 1, false>::occupancy}
 // First entry of each width is the default (chosen from the B200 measurements in DESIGN.md).
@@ -705,15 +709,16 @@ const Entry kTable[] = {
     KPM_VARIANT(4, 4, 4, kTiled, "tiled.lpr4.u4"),
     KPM_VARIANT(4, 4, 4, kDirect, "direct.lpr4.u4"),
     KPM_VARIANT(4, 4, 8, kDirect, "direct.lpr4.u8"),
+    KPM_VARIANT_WR_S(8, 4, 4, 2, "tiled.lpr4.u4.wr.s2"),
     KPM_VARIANT(8, 4, 4, kTiled, "tiled.lpr4.u4"),
     KPM_VARIANT(8, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kDirect, "direct.lpr8.u4"),
+    KPM_VARIANT_WR_S(16, 4, 4, 2, "tiled.lpr4.u4.wr.s2"),
     KPM_VARIANT(16, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(16, 4, 2, kTiled, "tiled.lpr4.u2"),
     KPM_VARIANT_WR(16, 8, 4, "tiled.lpr8.u4.wr"),
     KPM_VARIANT_CS(16, 8, 4, 2, "tiled.lpr8.u4.cs2"),
-    KPM_VARIANT(16, 16, 4, kTiled, "tiled.lpr16.u4.w16"),
     KPM_VARIANT(16, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(16, 8, 4, kDirect, "direct.lpr8.u4"),
     KPM_VARIANT(32, 8, 4, kTiled, "tiled.lpr8.u4"),
@@ -752,6 +757,11 @@ bool variant_staged(int R, int variant) {
 bool variant_tiled(int R, int variant) {
   const Entry* e = find(R, variant);
   return e && e->feed == kTiled;
+}
+
+int variant_stages(int R, int variant) {
+  const Entry* e = find(R, variant);
+  return e ? e->stages : 0;
 }
 
 bool variant_wstage(int R, int variant) {

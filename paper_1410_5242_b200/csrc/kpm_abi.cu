@@ -726,8 +726,9 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
 
   const int lg = __builtin_ctz(Rk);
   // tiled-feed plan (shared-memory layout + copy records) for one W placement
-  auto tiled_plan = [&](bool with_w, TileLayout& plan) -> kpm_status {
-    plan = s.tiles_ok ? plan_tiles(Rk, s.max_other, s.max_width, std::min(ctx->tile_stages, 4), with_w) : TileLayout();
+  auto tiled_plan = [&](bool with_w, int pref_stages, TileLayout& plan) -> kpm_status {
+    const int want = ctx->tile_stages ? std::min(ctx->tile_stages, 4) : pref_stages;
+    plan = s.tiles_ok ? plan_tiles(Rk, s.max_other, s.max_width, want, with_w) : TileLayout();
     const int ri = 2 * lg + (with_w ? 1 : 0);
     if (plan.stages >= 1 && !ctx->sell.rec[ri] && !ctx->sell.rec_failed[ri]) {
       size_t cap = 0;
@@ -746,7 +747,7 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   auto usable = [&](int v) {
     if (variant_tiled(Rk, v)) {
       TileLayout pl;
-      return tiled_plan(variant_wstage(Rk, v), pl) == KPM_OK && pl.stages >= 1;
+      return tiled_plan(variant_wstage(Rk, v), variant_stages(Rk, v), pl) == KPM_OK && pl.stages >= 1;
     }
     if (variant_staged(Rk, v)) return s.max_width <= staged_max_width();
     return true;
@@ -757,7 +758,9 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     for (variant = 0; variant < variant_count(Rk) - 1 && !usable(variant); ++variant) {
     }
   TileLayout plan;
-  if (variant_tiled(Rk, variant) && (st = tiled_plan(variant_wstage(Rk, variant), plan)) != KPM_OK) return st;
+  if (variant_tiled(Rk, variant) &&
+      (st = tiled_plan(variant_wstage(Rk, variant), variant_stages(Rk, variant), plan)) != KPM_OK)
+    return st;
   const int rec_index = 2 * lg + (variant_wstage(Rk, variant) ? 1 : 0);
   ctx->last_variant = variant_name(Rk, variant);
   const TileLayout tl = plan;

@@ -91,6 +91,7 @@ bool variant_tiled(int R, int variant);
 // Shared-memory plan of the tiled feed for block width R, or stages == 0 if it does not fit.
 TileLayout plan_tiles(int R, int64_t max_other, int64_t max_width, int stages, bool with_w);  // stages 0 = default
 bool variant_wstage(int R, int variant);  // tiled feed: old W staged in shared memory
+int variant_stages(int R, int variant);   // tiled feed: preferred ring depth (0 = default)
 cudaError_t launch_aug_spmmv(int R, int variant, bool init, const SweepArgs& a, int grid, cudaStream_t s);
 // eta[m][r] (double2) for m in [0, n_sweeps) from partials[m][3R][width] (width = launches x grid)
 cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int width, double2* eta_even,
