@@ -211,7 +211,10 @@ def main():
     import paper_1410_5242_b200 as kpm
 
     torch.cuda.set_device(local)
-    stream = torch.cuda.current_stream()
+    # one explicit stream: the library launches every kernel on it and the CUDA events that time
+    # the steps are recorded on it (the legacy default stream would hand the library its own)
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     dist = None
     if world > 1:
         import torch.distributed as dist
