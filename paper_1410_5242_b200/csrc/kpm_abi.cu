@@ -425,12 +425,45 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
   std::vector<char> reads_halo;    // per chunk, multi-rank planning
   auto alloc = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
 
-  if (H->mem == KPM_MEM_DEVICE && ctx->opt.sell_sigma == 1) {
-    // device build: the CSR never leaves the GPU (sell_device.cu)
+  // sigma = 1 builds on the device (sell_device.cu); a host CSR is staged to the device first
+  // (one H2D copy, then the same kernels), unless that does not fit or KPM_HOST_BUILD=1.
+  bool dev_build = ctx->opt.sell_sigma == 1 && env_int("KPM_HOST_BUILD", 0) == 0;
+  int64_t* st_rp = nullptr;
+  int64_t* st_col = nullptr;
+  double2* st_val = nullptr;
+  if (dev_build && H->mem == KPM_MEM_HOST) {
+    const int64_t nnz = H->row_ptr[n_loc];
+    if (H->row_ptr[0] != 0 || nnz < 0) return fail(ctx, KPM_EINVAL, "malformed row_ptr");
+    if (cudaMalloc(&st_rp, sizeof(int64_t) * (n_loc + 1)) != cudaSuccess ||
+        cudaMalloc(&st_col, sizeof(int64_t) * std::max<int64_t>(nnz, 1)) != cudaSuccess ||
+        cudaMalloc(&st_val, sizeof(double2) * std::max<int64_t>(nnz, 1)) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(st_rp);
+      cudaFree(st_col);
+      cudaFree(st_val);
+      st_rp = st_col = nullptr;
+      st_val = nullptr;
+      dev_build = false;  // not enough device memory for the staging copy: host build
+    } else {
+      KPM_CUDA(cudaMemcpyAsync(st_rp, H->row_ptr, sizeof(int64_t) * (n_loc + 1), cudaMemcpyHostToDevice, ctx->stream));
+      KPM_CUDA(cudaMemcpyAsync(st_col, H->col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+      KPM_CUDA(cudaMemcpyAsync(st_val, H->val, sizeof(double2) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+    }
+  }
+  if (dev_build) {
+    // device build: the CSR never leaves the GPU
     DeviceBuild db;
     std::string berr;
-    const int st = build_sell_device(H->row_ptr, H->col, reinterpret_cast<const double2*>(H->val), n_loc,
+    const bool staged = st_rp != nullptr;
+    const int st = build_sell_device(staged ? st_rp : H->row_ptr, staged ? st_col : H->col,
+                                     staged ? st_val : reinterpret_cast<const double2*>(H->val), n_loc,
                                      H->row_begin, H->row_end, H->n_global, d, db, berr, ctx->stream);
+    if (staged) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(st_rp);
+      cudaFree(st_col);
+      cudaFree(st_val);
+    }
     if (st) {
       free_sell(ctx->sell);
       cudaGetLastError();
@@ -881,7 +914,10 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   // into a CUDA graph per configuration and replayed (launch overhead matters for small
   // matrices, e.g. C1's 5-us sweeps); env KPM_GRAPH=0 launches them one by one.
   KPM_CUDA(cudaEventRecord(ctx->ev[1], str));
-  const bool use_graph = !multi && ctx->use_graph && n_sweeps > 2;
+  // graphs pay off only when a sweep is short (launch overhead ~ 4 us vs the sweep); for large
+  // matrices a re-capture after every kpm_set_matrix would cost more than it saves
+  const double sweep_bytes = 20.0 * (double)s.n_slots + 48.0 * Rk * (double)s.n_pad;
+  const bool use_graph = !multi && ctx->use_graph && n_sweeps > 2 && sweep_bytes < 512e6;
   if (use_graph) {
     const std::vector<int64_t> key = {Rk, variant, grid, n_sweeps, (int64_t)ctx->X0, (int64_t)ctx->X1,
                                       (int64_t)ctx->partials, (int64_t)sa.chunk_list, (int64_t)sa.rec,

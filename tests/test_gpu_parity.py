@@ -325,3 +325,19 @@ def test_optimisation_stages(pkg, stage):
         ctx.set_matrix(rp, col, val, a, b)
         mu, eta = ctx.moments_stage(stage, M, R, SEED)
     check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, M, R, SEED, mode=oracle.CHAINED))
+
+
+@pytest.mark.parametrize("sigma", [1, 64])
+def test_host_builder_forced(pkg, sigma, monkeypatch):
+    """KPM_HOST_BUILD=1 keeps the multithreaded host builder (the default for host input with
+    sigma = 1 is the device builder after one H2D copy): both give the reference SELL."""
+    monkeypatch.setenv("KPM_HOST_BUILD", "1")
+    lat, rp, col, val, a, b = problem((6, 5, 8))
+    with pkg.KpmContext(sell_sigma=sigma) as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        s = ctx.export_sell()
+        mu, eta = ctx.moments(40, 8, SEED)
+    ref = sell_ref.build_sell(rp, col, val, C=32, sigma=sigma)
+    for k in ("cptr", "col", "val", "perm"):
+        assert np.array_equal(s[k], ref[k]), k
+    check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, 40, 8, SEED))
