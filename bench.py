@@ -395,13 +395,18 @@ def main():
         out["e2e"] = None
         out["e2e_note"] = "C5 slabs (37 GB CSR per GPU) are generated on the device; no host-input e2e"
     elif not args.no_e2e:
+        pinned = [torch.from_numpy(x).pin_memory() for x in (rp, col, val)]  # the step's inputs, pinned host memory
+        prp, pcol, pval = (t.numpy() for t in pinned)
         h2d = rp.nbytes + col.nbytes + val.nbytes
         d2h = M * 8 + R * M * 16
+        ctx.set_matrix(prp, pcol, pval, a, b, n_global=n, row_begin=row_begin)  # warm-up: first DMA from these pages
+        if band:
+            apply_order()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            ctx.set_matrix(rp, col, val, a, b, n_global=n, row_begin=row_begin)
+            ctx.set_matrix(prp, pcol, pval, a, b, n_global=n, row_begin=row_begin)
             if band:
                 apply_order()
             ctx.moments(M, R, SEED, want_eta=True)

@@ -59,6 +59,10 @@ struct kpm_ctx {
   size_t v0_cap = 0;
   double2* u_naive = nullptr;  // naive stage's u vector
   size_t u_cap = 0;
+  int64_t* stage_rp = nullptr;  // device staging of a host CSR (device SELL build)
+  int64_t* stage_col = nullptr;
+  double2* stage_val = nullptr;
+  size_t stage_rp_cap = 0, stage_col_cap = 0, stage_val_cap = 0;
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
@@ -202,6 +206,9 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   cudaFree(ctx->eta_odd);
   cudaFree(ctx->v0_dev);
   cudaFree(ctx->u_naive);
+  cudaFree(ctx->stage_rp);
+  cudaFree(ctx->stage_col);
+  cudaFree(ctx->stage_val);
   if (ctx->h_eta) cudaFreeHost(ctx->h_eta);
   for (int i = 0; i < 4; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
@@ -249,12 +256,25 @@ static void free_sell(DevSell& s) {
   cudaFree(s.val);
   cudaFree(s.col);
   cudaFree(s.cptr);
-  cudaFree(s.perm);
+  cudaFree(s.perm_buf);
   cudaFree(s.lcol);
   cudaFree(s.nruns);
   cudaFree(s.runs);
   for (int i = 0; i < 12; ++i) cudaFree(s.rec[i]);
   s = DevSell();
+}
+
+// Forget the matrix but keep the device buffers for the next one (grow-only reuse).
+static void reset_sell(DevSell& s) {
+  DevSell k;
+  k.val = s.val, k.col = s.col, k.cptr = s.cptr, k.perm_buf = s.perm_buf, k.lcol = s.lcol, k.nruns = s.nruns, k.runs = s.runs;
+  k.val_cap = s.val_cap, k.col_cap = s.col_cap, k.cptr_cap = s.cptr_cap, k.perm_cap = s.perm_cap;
+  k.lcol_cap = s.lcol_cap, k.nruns_cap = s.nruns_cap, k.runs_cap = s.runs_cap;
+  for (int i = 0; i < 12; ++i) {
+    k.rec[i] = s.rec[i];
+    k.rec_cap[i] = s.rec_cap[i];
+  }
+  s = k;
 }
 
 // Halo exchange plan (collective): receive runs from the halo list, requests to the owners,
@@ -417,13 +437,12 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
     if (row_begins.back() != H->n_global) return fail(ctx, KPM_EINVAL, "row ranges do not cover n_global");
   }
 
-  free_sell(ctx->sell);
+  reset_sell(ctx->sell);
   ctx->have_matrix = false;
   DevSell& d = ctx->sell;
   std::vector<int64_t> halo;       // global ids of the halo slots
   std::vector<int32_t> perm_h;     // host perm (empty = identity)
   std::vector<char> reads_halo;    // per chunk, multi-rank planning
-  auto alloc = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
 
   // sigma = 1 builds on the device (sell_device.cu); a host CSR is staged to the device first
   // (one H2D copy, then the same kernels), unless that does not fit or KPM_HOST_BUILD=1.
@@ -434,17 +453,15 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
   if (dev_build && H->mem == KPM_MEM_HOST) {
     const int64_t nnz = H->row_ptr[n_loc];
     if (H->row_ptr[0] != 0 || nnz < 0) return fail(ctx, KPM_EINVAL, "malformed row_ptr");
-    if (cudaMalloc(&st_rp, sizeof(int64_t) * (n_loc + 1)) != cudaSuccess ||
-        cudaMalloc(&st_col, sizeof(int64_t) * std::max<int64_t>(nnz, 1)) != cudaSuccess ||
-        cudaMalloc(&st_val, sizeof(double2) * std::max<int64_t>(nnz, 1)) != cudaSuccess) {
+    if (reserve((void**)&ctx->stage_rp, &ctx->stage_rp_cap, sizeof(int64_t) * (n_loc + 1)) != cudaSuccess ||
+        reserve((void**)&ctx->stage_col, &ctx->stage_col_cap, sizeof(int64_t) * nnz) != cudaSuccess ||
+        reserve((void**)&ctx->stage_val, &ctx->stage_val_cap, sizeof(double2) * nnz) != cudaSuccess) {
       cudaGetLastError();
-      cudaFree(st_rp);
-      cudaFree(st_col);
-      cudaFree(st_val);
-      st_rp = st_col = nullptr;
-      st_val = nullptr;
       dev_build = false;  // not enough device memory for the staging copy: host build
     } else {
+      st_rp = ctx->stage_rp;
+      st_col = ctx->stage_col;
+      st_val = ctx->stage_val;
       KPM_CUDA(cudaMemcpyAsync(st_rp, H->row_ptr, sizeof(int64_t) * (n_loc + 1), cudaMemcpyHostToDevice, ctx->stream));
       KPM_CUDA(cudaMemcpyAsync(st_col, H->col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, ctx->stream));
       KPM_CUDA(cudaMemcpyAsync(st_val, H->val, sizeof(double2) * nnz, cudaMemcpyHostToDevice, ctx->stream));
@@ -458,14 +475,9 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
     const int st = build_sell_device(staged ? st_rp : H->row_ptr, staged ? st_col : H->col,
                                      staged ? st_val : reinterpret_cast<const double2*>(H->val), n_loc,
                                      H->row_begin, H->row_end, H->n_global, d, db, berr, ctx->stream);
-    if (staged) {
-      cudaStreamSynchronize(ctx->stream);
-      cudaFree(st_rp);
-      cudaFree(st_col);
-      cudaFree(st_val);
-    }
+    if (staged) cudaStreamSynchronize(ctx->stream);
     if (st) {
-      free_sell(ctx->sell);
+      reset_sell(ctx->sell);
       cudaGetLastError();
       if (st == 5) {
         ctx->sticky = true;
@@ -516,19 +528,20 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
     d.n_halo = hs.n_halo;
     d.max_width = 0;
     for (int64_t c = 0; c < hs.n_chunks; ++c) d.max_width = std::max(d.max_width, (hs.cptr[c + 1] - hs.cptr[c]) / hs.C);
-    cudaError_t e = alloc((void**)&d.val, sizeof(double2) * d.n_slots);
-    if (e == cudaSuccess) e = alloc((void**)&d.col, sizeof(int) * d.n_slots);
-    if (e == cudaSuccess) e = alloc((void**)&d.cptr, sizeof(int64_t) * (d.n_chunks + 1));
-    if (e == cudaSuccess && hs.sigma > 1) e = alloc((void**)&d.perm, sizeof(int) * d.n_loc);
+    cudaError_t e = reserve((void**)&d.val, &d.val_cap, sizeof(double2) * d.n_slots);
+    if (e == cudaSuccess) e = reserve((void**)&d.col, &d.col_cap, sizeof(int) * d.n_slots);
+    if (e == cudaSuccess) e = reserve((void**)&d.cptr, &d.cptr_cap, sizeof(int64_t) * (d.n_chunks + 1));
+    if (e == cudaSuccess && hs.sigma > 1) e = reserve((void**)&d.perm_buf, &d.perm_cap, sizeof(int) * d.n_loc);
+    if (e == cudaSuccess && hs.sigma > 1) d.perm = d.perm_buf;
     if (e != cudaSuccess) {
-      free_sell(ctx->sell);
+      reset_sell(ctx->sell);
       cudaGetLastError();
       return fail(ctx, KPM_ENOMEM, std::string("device allocation for the matrix failed: ") + cudaGetErrorString(e));
     }
     KPM_CUDA(cudaMemcpy(d.val, hs.val.data(), sizeof(double2) * d.n_slots, cudaMemcpyHostToDevice));
     KPM_CUDA(cudaMemcpy(d.col, hs.col.data(), sizeof(int) * d.n_slots, cudaMemcpyHostToDevice));
     KPM_CUDA(cudaMemcpy(d.cptr, hs.cptr.data(), sizeof(int64_t) * (d.n_chunks + 1), cudaMemcpyHostToDevice));
-    if (d.perm) {
+    if (hs.sigma > 1) {
       KPM_CUDA(cudaMemcpy(d.perm, hs.perm.data(), sizeof(int) * d.n_loc, cudaMemcpyHostToDevice));
       perm_h = hs.perm;
     }
@@ -547,9 +560,9 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
           rr[c * 2 * kMaxRuns + 2 * (k - t.run_ptr[c]) + 1] = t.runs[2 * k + 1];
         }
       }
-      if (alloc((void**)&d.lcol, sizeof(uint16_t) * t.lcol.size()) != cudaSuccess ||
-          alloc((void**)&d.nruns, sizeof(int) * nr.size()) != cudaSuccess ||
-          alloc((void**)&d.runs, sizeof(int) * rr.size()) != cudaSuccess) {
+      if (reserve((void**)&d.lcol, &d.lcol_cap, sizeof(uint16_t) * t.lcol.size()) != cudaSuccess ||
+          reserve((void**)&d.nruns, &d.nruns_cap, sizeof(int) * nr.size()) != cudaSuccess ||
+          reserve((void**)&d.runs, &d.runs_cap, sizeof(int) * rr.size()) != cudaSuccess) {
         cudaGetLastError();
         d.tiles_ok = false;  // the other feeds still work
       } else {
@@ -763,18 +776,19 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     const int want = ctx->tile_stages ? std::min(ctx->tile_stages, 4) : pref_stages;
     plan = s.tiles_ok ? plan_tiles(Rk, s.max_other, s.max_width, want, with_w) : TileLayout();
     const int ri = 2 * lg + (with_w ? 1 : 0);
-    if (plan.stages >= 1 && !ctx->sell.rec[ri] && !ctx->sell.rec_failed[ri]) {
-      size_t cap = 0;
-      kpm_status st2 = ensure(ctx, (void**)&ctx->sell.rec[ri], &cap, (size_t)kRecSlots * s.n_chunks, sizeof(uint4));
-      if (st2 != KPM_OK) {
+    if (plan.stages >= 1 && !ctx->sell.rec_valid[ri] && !ctx->sell.rec_failed[ri]) {
+      if (reserve((void**)&ctx->sell.rec[ri], &ctx->sell.rec_cap[ri], sizeof(uint4) * kRecSlots * s.n_chunks) !=
+          cudaSuccess) {
+        cudaGetLastError();
         ctx->sell.rec_failed[ri] = true;  // no memory for the records: another feed runs
         plan = TileLayout();
         return KPM_OK;
       }
       KPM_CUDA(launch_build_records(s.cptr, s.nruns, s.runs, s.n_chunks, Rk, plan.off_w, plan.off_val, plan.off_lcol,
                                     ctx->sell.rec[ri], ctx->stream));
+      ctx->sell.rec_valid[ri] = true;
     }
-    if (!ctx->sell.rec[ri]) plan = TileLayout();
+    if (!ctx->sell.rec_valid[ri]) plan = TileLayout();
     return KPM_OK;
   };
   auto usable = [&](int v) {

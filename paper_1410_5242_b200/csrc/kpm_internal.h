@@ -15,12 +15,26 @@ constexpr int kMaxBlockWidth = 32; // widest specialised block (R per batch)
 constexpr int kRecSlots = 16;      // copy-record slots per chunk (header + 15 bulk copies)
 constexpr int kMaxRuns = kRecSlots - 5;  // row runs per chunk (besides own rows, W, val, lcol)
 
+// Grow-only device allocation: reuse *p if it holds `bytes`, else reallocate (kpm_set_matrix is
+// called once per step in the e2e loop; large cudaFree/cudaMalloc pairs would dominate it).
+inline cudaError_t reserve(void** p, size_t* cap, size_t bytes) {
+  bytes = bytes < 16 ? 16 : bytes;
+  if (*p && *cap >= bytes) return cudaSuccess;
+  cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  const cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaSuccess) *cap = bytes;
+  return e;
+}
+
 // Device-side SELL-C-sigma matrix ("Data layout in HBM").
 struct DevSell {
   double2* val = nullptr;  // n_slots, chunk-column-major: entry j of row k of chunk c at cptr[c]+j*32+k
   int* col = nullptr;      // n_slots, int32 local column (position in the local+halo vector)
   int64_t* cptr = nullptr; // n_chunks+1
   int* perm = nullptr;     // n_loc: local row stored at position p (NULL: identity, sigma = 1)
+  int* perm_buf = nullptr; // grow-only storage behind perm
   int64_t n_loc = 0, n_pad = 0, n_chunks = 0, n_slots = 0, n_halo = 0;
   int64_t max_width = 0;   // widest chunk (entries per row)
   // tiled feed (TMA gather plan, see sell_build.h HostTiles)
@@ -30,7 +44,11 @@ struct DevSell {
   int* runs = nullptr;         // n_chunks x kMaxRuns x (first row, count)
   int64_t max_other = 0, max_runs = 0;
   uint4* rec[12] = {};        // copy records per (log2(R), W staged)
+  size_t rec_cap[12] = {};
+  bool rec_valid[12] = {};     // built for the current matrix
   bool rec_failed[12] = {};
+  // capacities (bytes) of the grow-only buffers above
+  size_t val_cap = 0, col_cap = 0, cptr_cap = 0, perm_cap = 0, lcol_cap = 0, nruns_cap = 0, runs_cap = 0;
 };
 
 // Shared-memory layout of one stage of the tiled feed (bytes, 128-B aligned sections).

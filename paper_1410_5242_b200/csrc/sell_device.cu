@@ -329,7 +329,7 @@ int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val,
   int64_t *w = nullptr, *slots = nullptr;
   DB_CUDA(cudaMalloc(&w, sizeof(int64_t) * n_chunks));
   DB_CUDA(cudaMalloc(&slots, sizeof(int64_t) * n_chunks));
-  DB_CUDA(cudaMalloc(&d.cptr, sizeof(int64_t) * (n_chunks + 1)));
+  DB_CUDA(reserve((void**)&d.cptr, &d.cptr_cap, sizeof(int64_t) * (n_chunks + 1)));
   width_kernel<<<grid_for(n_chunks, 256), 256, 0, s>>>(rp, n_loc, n_chunks, w, slots);
   DB_CUDA(cudaGetLastError());
   DB_CUDA(cudaMemsetAsync(d.cptr, 0, sizeof(int64_t), s));
@@ -395,16 +395,16 @@ int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val,
   DB_CUDA(cudaStreamSynchronize(s));
 
   // scatter
-  DB_CUDA(cudaMalloc(&d.val, sizeof(double2) * std::max<int64_t>(1, d.n_slots)));
-  DB_CUDA(cudaMalloc(&d.col, sizeof(int) * std::max<int64_t>(1, d.n_slots)));
+  DB_CUDA(reserve((void**)&d.val, &d.val_cap, sizeof(double2) * d.n_slots));
+  DB_CUDA(reserve((void**)&d.col, &d.col_cap, sizeof(int) * d.n_slots));
   scatter_kernel<<<grid_for(n_chunks * 32, 256), 256, 0, s>>>(rp, col, val, n_loc, n_chunks, row_begin, row_end,
                                                                n_pad, halo, n_halo, d.cptr, d.val, d.col);
   DB_CUDA(cudaGetLastError());
 
   // tile plan
-  DB_CUDA(cudaMalloc(&d.lcol, sizeof(uint16_t) * std::max<int64_t>(1, d.n_slots)));
-  DB_CUDA(cudaMalloc(&d.nruns, sizeof(int) * n_chunks));
-  DB_CUDA(cudaMalloc(&d.runs, sizeof(int) * 2 * kMaxRuns * n_chunks));
+  DB_CUDA(reserve((void**)&d.lcol, &d.lcol_cap, sizeof(uint16_t) * d.n_slots));
+  DB_CUDA(reserve((void**)&d.nruns, &d.nruns_cap, sizeof(int) * n_chunks));
+  DB_CUDA(reserve((void**)&d.runs, &d.runs_cap, sizeof(int) * 2 * kMaxRuns * n_chunks));
   int* nother = nullptr;
   DB_CUDA(cudaMalloc(&nother, sizeof(int) * n_chunks));
   DB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), s));
