@@ -128,6 +128,22 @@ kpm_status kpm_moments_v0(kpm_ctx* ctx, int M, int R, const double* v0, double* 
 enum { KPM_STAGE_NAIVE = 0, KPM_STAGE_AUG_SPMV = 1, KPM_STAGE_AUG_SPMMV = 2 };
 kpm_status kpm_moments_stage(kpm_ctx* ctx, int stage, int M, int R, uint64_t seed, double* mu, double* eta);
 
+/* The paper's bottleneck-analysis kernels (Figs. 8-9): run n_sweeps (>= 1) of one
+ * kernel kind at block width R (1, 2, 4, 8, 16 or 32) on the current matrix, single rank
+ * (KPM_ESTATE otherwise, or if the matrix does not fit the tiled feed):
+ *   KPM_SWEEP_AUG        the fully augmented sweep of kpm_moments (dots computed, discarded),
+ *   KPM_SWEEP_AUG_NODOT  the same without the on-the-fly dot products,
+ *   KPM_SWEEP_SPMMV      the plain SpMMV  W = H V.
+ * V = the Z4 block of kpm_moments(seed) (columns 0..R-1), W = 0 before the first sweep; every
+ * sweep reads the same V (no swap), so the augmented kinds leave W = 2a(H - b)V after an odd
+ * number of sweeps and 0 after an even one.
+ *   ms_per_sweep  out (NULL to skip): average device time of one sweep (CUDA events).
+ *   w_out         out (NULL to skip), host: the final W, n_loc x R row-major complex, local
+ *                 row order (2*n_loc*R doubles). */
+enum { KPM_SWEEP_AUG = 0, KPM_SWEEP_AUG_NODOT = 1, KPM_SWEEP_SPMMV = 2 };
+kpm_status kpm_sweep_kernel(kpm_ctx* ctx, int kind, int R, uint64_t seed, int n_sweeps, double* ms_per_sweep,
+                            double* w_out);
+
 /* Device time of the last kpm_moments* call, measured with CUDA events on the context's
  * stream: total_ms = start-vector init .. last eta reduction; sweep_ms = average duration
  * of one main aug_spmmv sweep (the hot kernel); n_sweeps = main sweeps timed. */

@@ -22,7 +22,7 @@ STATUS_NAMES = ["KPM_OK", "KPM_EINVAL", "KPM_ESTATE", "KPM_ERANGE", "KPM_ENOMEM"
 # exported symbols declared in include/kpm.h
 ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_dos", "kpm_export_sell", "kpm_get_sell_info", "kpm_get_unique_id",
                "kpm_last_error", "kpm_last_kernel", "kpm_last_timing", "kpm_moments", "kpm_moments_stage", "kpm_moments_v0",
-               "kpm_plan_recv", "kpm_plan_send", "kpm_set_chunk_order", "kpm_set_matrix"]
+               "kpm_plan_recv", "kpm_plan_send", "kpm_set_chunk_order", "kpm_set_matrix", "kpm_sweep_kernel"]
 
 
 class KpmError(RuntimeError):
@@ -66,6 +66,7 @@ def load_library():
     lib.kpm_moments.argtypes = [P, i32, i32, u64, P, P]
     lib.kpm_moments_v0.argtypes = [P, i32, i32, P, P, P]
     lib.kpm_moments_stage.argtypes = [P, i32, i32, i32, u64, P, P]
+    lib.kpm_sweep_kernel.argtypes = [P, i32, i32, u64, i32, P, P]
     lib.kpm_last_timing.argtypes = [P, P, P, P]
     lib.kpm_get_sell_info.argtypes = [P, ctypes.POINTER(kpm_sell_info)]
     lib.kpm_export_sell.argtypes = [P, P, P, P, P, P]
@@ -216,6 +217,15 @@ class KpmContext:
         eta = np.zeros((R, M), dtype=np.complex128) if want_eta else None
         self._check(self.lib.kpm_moments_stage(self.h, code, M, R, seed, _ptr(mu), _ptr(eta)), (KPM_WDIVERGED,))
         return mu, eta
+
+    def sweep_kernel(self, kind, R, seed, n_sweeps=1, want_w=False):
+        """kpm_sweep_kernel: time n_sweeps of 'aug', 'aug_nodot' or 'spmmv' (the paper's Fig. 9
+        kernels) at block width R; returns (ms per sweep, W (n_loc, R) complex or None)."""
+        code = {"aug": 0, "aug_nodot": 1, "spmmv": 2}[kind]
+        ms = ctypes.c_double(0.0)
+        w = np.zeros((self.sell_info().n_loc, R), dtype=np.complex128) if want_w else None
+        self._check(self.lib.kpm_sweep_kernel(self.h, code, R, seed, n_sweeps, ctypes.byref(ms), _ptr(w)))
+        return ms.value, w
 
     def moments_v0(self, M, v0, allow=(KPM_WDIVERGED,)):
         v0 = np.ascontiguousarray(v0, dtype=np.complex128)

@@ -426,6 +426,7 @@ __global__ void eta_finalize_kernel(const double* __restrict__ partials, int n_s
 // so every gathered V row is fetched from L2/HBM once per chunk and no gather occupies a
 // register while in flight.  All warps then compute from shared memory.
 constexpr int kMaxTileStages = 4;
+enum SweepKind { kAug = 0, kAugNoDot = 1, kSpmmv = 2 };  // = KPM_SWEEP_* in kpm.h
 constexpr int kTileBudget = 232448 - 8192;  // minus static smem (reduction buffer, barriers)  // 227 KB dynamic shared memory minus margin
 
 // CS = column split: CS consumer warps share a row group, each owning CPL/CS of the lane's
@@ -439,7 +440,11 @@ __host__ __device__ constexpr int tiled_threads() { return 32 * (tiled_ncwg<LPR>
 
 // WS: the old W rows travel in the tile (TMA) or, WS = false, straight into registers (LDG,
 // streaming) -- a smaller stage, so more CTAs fit per SM.
-template <int R, int LPR, int U, int CS, bool WS, bool INIT>
+// KIND: the paper's three kernels of the bottleneck analysis (Fig. 9):
+//   kAug       the fully augmented SpMMV of Fig. 5 (the hot path),
+//   kAugNoDot  the same without the on-the-fly dot products,
+//   kSpmmv     the plain SpMMV W = H V (no shift/scale, no old W).
+template <int R, int LPR, int U, int CS, bool WS, bool INIT, int KIND = kAug>
 __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(const SweepArgs a) {
   using Cf = Cfg<R, LPR, U>;
   constexpr int RW = Cf::RW, G = kC / RW;
@@ -448,6 +453,8 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
   constexpr int NCWG = tiled_ncwg<LPR>(); // consumer warps per column part
   constexpr int NCW = NCWG * CS;          // consumer warps
   constexpr int kTiledThreads = tiled_threads<LPR, CS>();
+  constexpr bool NEED_W = !INIT && KIND != kSpmmv;  // the recurrence's "- W" term
+  constexpr bool W_TILE = NEED_W && WS;             // old W rows staged in the tile
   extern __shared__ __align__(128) unsigned char tsm[];
   __shared__ __align__(8) uint64_t full[kMaxTileStages], empty[kMaxTileStages];
   __shared__ int tile_len[kMaxTileStages];
@@ -486,7 +493,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
         nxt = lane < 16 ? __ldg(a.rec + c_nxt * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
       }
       const int s = (int)(k % tl.stages);
-      const uint32_t total = __shfl_sync(0xffffffffu, (INIT || !WS) ? cur.y : cur.x, 0);
+      const uint32_t total = __shfl_sync(0xffffffffu, W_TILE ? cur.x : cur.y, 0);
       const uint32_t L = __shfl_sync(0xffffffffu, cur.z, 0);
       const uint32_t ncmd = __shfl_sync(0xffffffffu, cur.w, 0);
       if (k >= tl.stages) mbar_wait(smem_u32(&empty[s]), (uint32_t)(((k / tl.stages) - 1) & 1));
@@ -502,7 +509,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
       if (lane >= 1 && (uint32_t)lane <= ncmd) {
         const uint32_t base = cur.w >> 28, bytes = cur.w & 0x0FFFFFFFu;
         const int64_t off = (int64_t)(((uint64_t)cur.y << 32) | cur.x);
-        if (!((INIT || !WS) && base == 1)) {
+        if (W_TILE || base != 1) {
           const unsigned char* src = base == 0   ? reinterpret_cast<const unsigned char*>(a.V)
                                      : base == 1 ? reinterpret_cast<const unsigned char*>(a.W)
                                      : base == 2 ? reinterpret_cast<const unsigned char*>(a.val)
@@ -535,7 +542,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
         const int kr = gq * RW + q;
         const int64_t p = c * kC + kr;
         double2 wreg[CPL];
-        if (!WS && !INIT && p < a.n_loc) {  // old W straight from HBM, lands under the gathers
+        if (NEED_W && !WS && p < a.n_loc) {  // old W straight from HBM, lands under the gathers
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) wreg[cc] = ld_stream(a.W + p * R + (cc ^ sw) * LPR + t, pol);
         }
@@ -574,6 +581,10 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) {
             const int col = (cc ^ sw) * LPR + t;
+            if (KIND == kSpmmv) {
+              st_stream(a.W + p * R + col, u[cc], pol);
+              continue;
+            }
             const double2 vi = sV[kr * R + col];
             double2 uu = u[cc];
             uu.x = fma(-a.b, vi.x, uu.x);
@@ -587,9 +598,11 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
             }
             st_stream(a.W + p * R + col, w, pol);
             store_peers<R>(a, p, col, w);
-            d.ee[cc] = fma(vi.x, vi.x, fma(vi.y, vi.y, d.ee[cc]));
-            d.eor[cc] = fma(w.x, vi.x, fma(w.y, vi.y, d.eor[cc]));
-            d.eoi[cc] = fma(w.x, vi.y, fma(-w.y, vi.x, d.eoi[cc]));
+            if (KIND == kAug) {
+              d.ee[cc] = fma(vi.x, vi.x, fma(vi.y, vi.y, d.ee[cc]));
+              d.eor[cc] = fma(w.x, vi.x, fma(w.y, vi.y, d.eor[cc]));
+              d.eoi[cc] = fma(w.x, vi.y, fma(-w.y, vi.x, d.eoi[cc]));
+            }
           }
         }
       }
@@ -597,7 +610,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
       if (lane == 0) mbar_arrive(smem_u32(&empty[s]));  // stage s released by this warp
     }
     // undo the swizzle so that accumulator cc holds column block cc on every lane
-    if (SWR > 1) {
+    if (SWR > 1 && KIND == kAug) {
       Dots<CPL> e = d;
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc)
@@ -611,7 +624,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
     }
     // warp-level part of the dot-product reduction
 #pragma unroll
-    for (int off = LPR; off < 32; off <<= 1) {
+    for (int off = LPR; off < (KIND == kAug ? 32 : 0); off <<= 1) {
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) {
         d.ee[cc] += __shfl_xor_sync(0xffffffffu, d.ee[cc], off);
@@ -619,7 +632,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
         d.eoi[cc] += __shfl_xor_sync(0xffffffffu, d.eoi[cc], off);
       }
     }
-    if (lane < LPR) {
+    if (KIND == kAug && lane < LPR) {
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) {
         const int r = cc * LPR + t;
@@ -629,6 +642,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
       }
     }
   }
+  if (KIND != kAug) return;
   __syncthreads();
   for (int i = tid; i < 3 * R; i += kTiledThreads) {
     double sum = 0.0;
@@ -706,7 +720,11 @@ const Entry kTable[] = {
     KPM_VARIANT(2, 2, 4, kTiled, "tiled.lpr2.u4"),
     KPM_VARIANT(2, 2, 4, kDirect, "direct.lpr2.u4"),
     KPM_VARIANT(2, 2, 8, kDirect, "direct.lpr2.u8"),
+    KPM_VARIANT_WR(4, 4, 4, "tiled.lpr4.u4.wr"),
     KPM_VARIANT(4, 4, 4, kTiled, "tiled.lpr4.u4"),
+    KPM_VARIANT_WR_S(4, 4, 4, 2, "tiled.lpr4.u4.wr.s2"),
+    KPM_VARIANT(4, 2, 4, kTiled, "tiled.lpr2.u4"),
+    KPM_VARIANT(4, 4, 2, kTiled, "tiled.lpr4.u2"),
     KPM_VARIANT(4, 4, 4, kDirect, "direct.lpr4.u4"),
     KPM_VARIANT(4, 4, 8, kDirect, "direct.lpr4.u8"),
     KPM_VARIANT_WR_S(8, 4, 4, 2, "tiled.lpr4.u4.wr.s2"),
@@ -718,6 +736,8 @@ const Entry kTable[] = {
     KPM_VARIANT(16, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(16, 4, 2, kTiled, "tiled.lpr4.u2"),
     KPM_VARIANT_WR(16, 8, 4, "tiled.lpr8.u4.wr"),
+    KPM_VARIANT_WR(16, 4, 4, "tiled.lpr4.u4.wr"),
+    KPM_VARIANT_WR_S(16, 8, 4, 2, "tiled.lpr8.u4.wr.s2"),
     KPM_VARIANT_CS(16, 8, 4, 2, "tiled.lpr8.u4.cs2"),
     KPM_VARIANT(16, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(16, 8, 4, kDirect, "direct.lpr8.u4"),
@@ -801,6 +821,40 @@ cudaError_t launch_aug_spmmv(int R, int variant, bool init, const SweepArgs& a, 
   const Entry* e = find(R, variant);
   if (!e) return cudaErrorInvalidValue;
   return e->launch(init, a, grid, s);
+}
+
+// Bottleneck-analysis kernels (KPM_SWEEP_AUG_NODOT / KPM_SWEEP_SPMMV): the default tiled
+// variant of each width (first kTable entry) with the dots, or also the shift/scale/-W, removed.
+namespace {
+template <int R, int LPR, bool WS, int KIND>
+cudaError_t launch_kind(const SweepArgs& a, int grid, cudaStream_t s) {
+  const int smem = a.tl.stages * a.tl.stage_bytes;
+  cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, 4, 1, WS, false, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  aug_spmmv_tiled<R, LPR, 4, 1, WS, false, KIND><<<grid, tiled_threads<LPR, 1>(), smem, s>>>(a);
+  return cudaGetLastError();
+}
+typedef cudaError_t (*KindFn)(const SweepArgs&, int, cudaStream_t);
+struct KindEntry {
+  int R;
+  KindFn nodot, spmmv;
+};
+// keep in step with the defaults at the head of each width in kTable
+const KindEntry kKinds[] = {
+    {1, launch_kind<1, 1, true, kAugNoDot>, launch_kind<1, 1, true, kSpmmv>},
+    {2, launch_kind<2, 2, true, kAugNoDot>, launch_kind<2, 2, true, kSpmmv>},
+    {4, launch_kind<4, 4, false, kAugNoDot>, launch_kind<4, 4, false, kSpmmv>},
+    {8, launch_kind<8, 4, false, kAugNoDot>, launch_kind<8, 4, false, kSpmmv>},
+    {16, launch_kind<16, 4, false, kAugNoDot>, launch_kind<16, 4, false, kSpmmv>},
+    {32, launch_kind<32, 8, true, kAugNoDot>, launch_kind<32, 8, true, kSpmmv>},
+};
+}  // namespace
+
+cudaError_t launch_sweep_kind(int R, int kind, const SweepArgs& a, int grid, cudaStream_t s) {
+  if (kind == kAug) return launch_aug_spmmv(R, 0, false, a, grid, s);
+  if (!variant_tiled(R, 0)) return cudaErrorInvalidValue;
+  for (const KindEntry& e : kKinds)
+    if (e.R == R) return kind == kAugNoDot ? e.nodot(a, grid, s) : kind == kSpmmv ? e.spmmv(a, grid, s) : cudaErrorInvalidValue;
+  return cudaErrorInvalidValue;
 }
 
 static int elementwise_grid(int64_t n_el) {

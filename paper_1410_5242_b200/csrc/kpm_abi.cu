@@ -734,6 +734,29 @@ static kpm_status setup_fused(kpm_ctx* ctx, int Rk) {
 
 // One block of up to 32 columns: start block, M/2 sweeps, eta reduction, D2H.
 // eta_cols: host, [(r*M + n)] double2 for the rb columns of this block.
+// Tiled-feed plan (shared-memory layout + copy records, built once per matrix) for block width
+// Rk and one W placement; plan.stages == 0 if the matrix does not fit the tiled feed.
+static kpm_status plan_tiled_feed(kpm_ctx* ctx, int Rk, bool with_w, int pref_stages, TileLayout& plan) {
+  const DevSell& s = ctx->sell;
+  const int want = ctx->tile_stages ? std::min(ctx->tile_stages, 4) : pref_stages;
+  plan = s.tiles_ok ? plan_tiles(Rk, s.max_other, s.max_width, want, with_w) : TileLayout();
+  const int ri = 2 * __builtin_ctz(Rk) + (with_w ? 1 : 0);
+  if (plan.stages >= 1 && !ctx->sell.rec_valid[ri] && !ctx->sell.rec_failed[ri]) {
+    if (reserve((void**)&ctx->sell.rec[ri], &ctx->sell.rec_cap[ri], sizeof(uint4) * kRecSlots * s.n_chunks) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      ctx->sell.rec_failed[ri] = true;  // no memory for the records: another feed runs
+      plan = TileLayout();
+      return KPM_OK;
+    }
+    KPM_CUDA(launch_build_records(s.cptr, s.nruns, s.runs, s.n_chunks, Rk, plan.off_w, plan.off_val, plan.off_lcol,
+                                  ctx->sell.rec[ri], ctx->stream));
+    ctx->sell.rec_valid[ri] = true;
+  }
+  if (!ctx->sell.rec_valid[ri]) plan = TileLayout();
+  return KPM_OK;
+}
+
 static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint64_t seed, const double* v0,
                             double2* eta_cols, bool first, bool last) {
   const int Rk = block_width(rb);
@@ -771,25 +794,8 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   }
 
   const int lg = __builtin_ctz(Rk);
-  // tiled-feed plan (shared-memory layout + copy records) for one W placement
-  auto tiled_plan = [&](bool with_w, int pref_stages, TileLayout& plan) -> kpm_status {
-    const int want = ctx->tile_stages ? std::min(ctx->tile_stages, 4) : pref_stages;
-    plan = s.tiles_ok ? plan_tiles(Rk, s.max_other, s.max_width, want, with_w) : TileLayout();
-    const int ri = 2 * lg + (with_w ? 1 : 0);
-    if (plan.stages >= 1 && !ctx->sell.rec_valid[ri] && !ctx->sell.rec_failed[ri]) {
-      if (reserve((void**)&ctx->sell.rec[ri], &ctx->sell.rec_cap[ri], sizeof(uint4) * kRecSlots * s.n_chunks) !=
-          cudaSuccess) {
-        cudaGetLastError();
-        ctx->sell.rec_failed[ri] = true;  // no memory for the records: another feed runs
-        plan = TileLayout();
-        return KPM_OK;
-      }
-      KPM_CUDA(launch_build_records(s.cptr, s.nruns, s.runs, s.n_chunks, Rk, plan.off_w, plan.off_val, plan.off_lcol,
-                                    ctx->sell.rec[ri], ctx->stream));
-      ctx->sell.rec_valid[ri] = true;
-    }
-    if (!ctx->sell.rec_valid[ri]) plan = TileLayout();
-    return KPM_OK;
+  auto tiled_plan = [&](bool with_w, int pref_stages, TileLayout& plan) {
+    return plan_tiled_feed(ctx, Rk, with_w, pref_stages, plan);
   };
   auto usable = [&](int v) {
     if (variant_tiled(Rk, v)) {
@@ -1144,6 +1150,84 @@ extern "C" kpm_status kpm_moments_stage(kpm_ctx* ctx, int stage, int M, int R, u
 extern "C" kpm_status kpm_moments_v0(kpm_ctx* ctx, int M, int R, const double* v0, double* mu, double* eta) {
   if (ctx && !v0) return fail(ctx, KPM_EINVAL, "v0 is NULL");
   return moments_common(ctx, M, R, 0, v0, mu, eta);
+}
+
+extern "C" kpm_status kpm_sweep_kernel(kpm_ctx* ctx, int kind, int R, uint64_t seed, int n_sweeps,
+                                       double* ms_per_sweep, double* w_out) {
+  if (!ctx) return KPM_EINVAL;
+  if (ctx->sticky) return fail(ctx, KPM_ESTATE, "context has a sticky CUDA/NCCL error: " + ctx->err);
+  if (!ctx->have_matrix) return fail(ctx, KPM_ESTATE, "kpm_set_matrix has not been called");
+  if (ctx->opt.nranks > 1) return fail(ctx, KPM_ESTATE, "kpm_sweep_kernel is single-rank");
+  if (kind < KPM_SWEEP_AUG || kind > KPM_SWEEP_SPMMV) return fail(ctx, KPM_EINVAL, "unknown sweep kind");
+  if (R < 1 || R > kMaxBlockWidth || (R & (R - 1))) return fail(ctx, KPM_EINVAL, "R must be 1, 2, 4, 8, 16 or 32");
+  if (n_sweeps < 1) return fail(ctx, KPM_EINVAL, "n_sweeps must be >= 1");
+  KPM_CUDA(cudaSetDevice(ctx->opt.device));
+  const DevSell& s = ctx->sell;
+  const int64_t n_rows_total = s.n_pad + s.n_halo;
+  kpm_status st;
+  size_t xcap = ctx->x_cap;
+  if ((st = ensure(ctx, (void**)&ctx->X0, &xcap, (size_t)n_rows_total * R, sizeof(double2))) != KPM_OK) return st;
+  xcap = ctx->x_cap;
+  if ((st = ensure(ctx, (void**)&ctx->X1, &xcap, (size_t)n_rows_total * R, sizeof(double2))) != KPM_OK) return st;
+  ctx->x_cap = xcap;
+  TileLayout tl;
+  if (variant_tiled(R, 0) && (st = plan_tiled_feed(ctx, R, variant_wstage(R, 0), variant_stages(R, 0), tl)) != KPM_OK)
+    return st;
+  if (!variant_tiled(R, 0) || tl.stages < 1)
+    return fail(ctx, KPM_ESTATE, "the matrix does not fit the tiled feed of the analysis kernels");
+  const int dyn_smem = tl.stages * tl.stage_bytes;
+  const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, sweep_occupancy(R, 0, dyn_smem));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * occ, s.n_chunks));
+  if ((st = ensure(ctx, (void**)&ctx->partials, &ctx->partials_cap, (size_t)3 * R * grid, sizeof(double))) != KPM_OK)
+    return st;
+  cudaStream_t str = ctx->stream;
+  KPM_CUDA(launch_z4_init(ctx->X0, ctx->X1, s.perm, s.n_loc, s.n_pad, ctx->halo_rows, n_rows_total, R, ctx->row_begin, 0,
+                          R, seed, str));
+  SweepArgs sa;
+  sa.val = s.val;
+  sa.col = s.col;
+  sa.cptr = s.cptr;
+  sa.n_loc = s.n_loc;
+  sa.chunk_list = ctx->order_list;
+  sa.chunk_begin = 0;
+  sa.chunk_end = s.n_chunks;
+  sa.rec = s.rec[2 * __builtin_ctz(R) + (variant_wstage(R, 0) ? 1 : 0)];
+  sa.lcol = s.lcol;
+  sa.tl = tl;
+  sa.b = ctx->b;
+  sa.scale = 2.0 * ctx->a;
+  sa.V = ctx->X0;
+  sa.W = ctx->X1;
+  sa.partials = ctx->partials;
+  sa.pstride = grid;
+  sa.n_peer = 0;
+  sa.v_evict_last = env_int("KPM_V_EVICT_LAST", 1);
+  KPM_CUDA(cudaEventRecord(ctx->ev[1], str));
+  for (int i = 0; i < n_sweeps; ++i) KPM_CUDA(launch_sweep_kind(R, kind, sa, grid, str));
+  KPM_CUDA(cudaEventRecord(ctx->ev[2], str));
+  KPM_CUDA(cudaStreamSynchronize(str));
+  float ms = 0.f;
+  KPM_CUDA(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]));
+  if (ms_per_sweep) *ms_per_sweep = ms / n_sweeps;
+  static const char* kSuffix[] = {"", ".nodot", ".spmmv"};
+  ctx->last_variant = std::string(variant_name(R, 0)) + kSuffix[kind];
+  if (w_out) {  // stored position p holds local row perm[p] (identity when sigma = 1)
+    std::vector<double2> wh((size_t)s.n_pad * R);
+    KPM_CUDA(cudaMemcpy(wh.data(), ctx->X1, sizeof(double2) * wh.size(), cudaMemcpyDeviceToHost));
+    std::vector<int> perm;
+    if (s.perm) {
+      perm.resize(s.n_loc);
+      KPM_CUDA(cudaMemcpy(perm.data(), s.perm, sizeof(int) * s.n_loc, cudaMemcpyDeviceToHost));
+    }
+    for (int64_t p = 0; p < s.n_loc; ++p) {
+      const int64_t row = s.perm ? perm[p] : p;
+      for (int r = 0; r < R; ++r) {
+        w_out[2 * (row * R + r)] = wh[(size_t)p * R + r].x;
+        w_out[2 * (row * R + r) + 1] = wh[(size_t)p * R + r].y;
+      }
+    }
+  }
+  return KPM_OK;
 }
 
 extern "C" kpm_status kpm_last_timing(const kpm_ctx* ctx, double* total_ms, double* sweep_ms, int* n_sweeps) {

@@ -341,3 +341,51 @@ def test_host_builder_forced(pkg, sigma, monkeypatch):
     for k in ("cptr", "col", "val", "perm"):
         assert np.array_equal(s[k], ref[k]), k
     check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, 40, 8, SEED))
+
+
+@pytest.mark.parametrize("R", [1, 4, 8, 16, 32])
+@pytest.mark.parametrize("kind", ["spmmv", "aug_nodot", "aug"])
+def test_analysis_kernels(pkg, kind, R):
+    """kpm_sweep_kernel (the paper's three kernels of the bottleneck analysis):
+    W = H V for the plain SpMMV; W = 2a(H - b)V after one augmented sweep from W = 0; after
+    two, W = fma(2a, u, -W1) = the rounding residual of W1 (|.| <= ulp/2), and after three
+    round(2a u - residual) = W1 exactly.  V = the oracle's Z4 block;
+    H V by scipy.sparse (a library product, not the kernel's arithmetic)."""
+    import scipy.sparse as sp
+
+    lat, rp, col, val, a, b = problem((6, 5, 7))  # ragged last chunk
+    V = oracle.z4_block(0, lat.n, 0, R, SEED)
+    HV = sp.csr_matrix((val, col, rp), shape=(lat.n, lat.n)) @ V
+    want = HV if kind == "spmmv" else 2 * a * (HV - b * V)
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        ms, w1 = ctx.sweep_kernel(kind, R, SEED, n_sweeps=1, want_w=True)
+        assert ms > 0
+        assert ctx.last_kernel().endswith({"spmmv": ".spmmv", "aug_nodot": ".nodot", "aug": ""}[kind])
+        _, w2 = ctx.sweep_kernel(kind, R, SEED, n_sweeps=2, want_w=True)
+        _, w3 = ctx.sweep_kernel(kind, R, SEED, n_sweeps=3, want_w=True)
+    scale = np.max(np.abs(want))
+    assert np.max(np.abs(w1 - want)) <= 1e-13 * scale
+    if kind == "spmmv":
+        assert np.array_equal(w2, w1) and np.array_equal(w3, w1)
+    else:
+        assert np.max(np.abs(w2)) <= 2.0 ** -52 * scale and np.array_equal(w3, w1)
+
+
+def test_analysis_kernel_errors(pkg):
+    lat, rp, col, val, a, b = problem((4, 4, 4))
+    with pkg.KpmContext() as ctx:
+        with pytest.raises(pkg.KpmError) as e:
+            ctx.sweep_kernel("spmmv", 8, SEED)
+        assert e.value.status == pkg.KPM_ESTATE
+        ctx.set_matrix(rp, col, val, a, b)
+        for R in (0, 3, 64):
+            with pytest.raises(pkg.KpmError) as e:
+                ctx.sweep_kernel("aug", R, SEED)
+            assert e.value.status == pkg.KPM_EINVAL
+        with pytest.raises(pkg.KpmError) as e:
+            ctx.sweep_kernel("aug", 8, SEED, n_sweeps=0)
+        assert e.value.status == pkg.KPM_EINVAL
+        assert ctx.lib.kpm_sweep_kernel(ctx.h, 7, 8, SEED, 1, None, None) == pkg.KPM_EINVAL  # unknown kind
+        mu, _ = ctx.moments(16, 4, SEED)  # context still usable
+        assert mu[0] == lat.n
