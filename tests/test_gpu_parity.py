@@ -389,3 +389,26 @@ def test_analysis_kernel_errors(pkg):
         assert ctx.lib.kpm_sweep_kernel(ctx.h, 7, 8, SEED, 1, None, None) == pkg.KPM_EINVAL  # unknown kind
         mu, _ = ctx.moments(16, 4, SEED)  # context still usable
         assert mu[0] == lat.n
+
+
+def test_c3_full_size_partial_bloch(pkg):
+    """Full C3 size (200x100x40, N = 3.2M) at V = 0 against the exact spectrum (SURVEY §8(c)
+    "open-z, large N"): with Z4 vectors E[m_n] = tr T_n(H~) and Var(m_n) = sum_{i!=j}
+    |T_n(H~)_ij|^2 <= ||T_n(H~)||_F^2 = sum_k T_n(x_k)^2, so every mu_n must lie within 6 of
+    these (upper-bound) standard deviations of the exact trace; a dropped term, sign or
+    scale error moves mu_n by O(N) >> sigma ~ sqrt(N/R).  mu_0 = N exactly."""
+    from bloch_ref import cheb_moments, slab_energies
+
+    lat, rp, col, val, a, b = problem((200, 100, 40), potential=ZERO_POTENTIAL)
+    M, R = 200, 32
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, _ = ctx.moments(M, R, SEED, want_eta=False)
+    x = a * (slab_energies(lat, rp, col, val) - b)
+    assert np.max(np.abs(x)) < 1
+    tr, sq = cheb_moments(x, M)
+    sigma = np.sqrt(sq / R)
+    z = np.abs(mu - tr) / sigma
+    assert mu[0] == lat.n
+    assert np.max(z[1:]) < 6.0, (np.argmax(z), np.max(z))
+    assert np.sqrt(np.mean(z[1:] ** 2)) < 1.5

@@ -141,3 +141,17 @@ def test_halo_lists_xslab():
         assert np.array_equal(halo[owner == right], np.arange(row_begins[right], row_begins[right] + lp))
     sl = sell_ref.send_lists(cols_by_rank, row_begins)
     assert len(sl) == 2 * P
+
+
+def test_slab_bloch_spectrum_matches_dense():
+    """tests/bloch_ref.py (open z, periodic x, y, V = 0) against dense eigvalsh."""
+    import scipy.sparse as sp
+
+    from bloch_ref import slab_energies
+
+    for dims in ((6, 5, 4), (4, 7, 3)):
+        lat = Lattice(*dims, potential=ZERO_POTENTIAL)
+        rp, col, val = generate_csr(lat)
+        e = np.sort(slab_energies(lat, rp, col, val, workers=2))
+        ed = np.linalg.eigvalsh(sp.csr_matrix((val, col, rp), shape=(lat.n, lat.n)).toarray())
+        assert np.max(np.abs(e - ed)) < 1e-12
