@@ -66,8 +66,15 @@ typedef struct {
                                    is supported                                             */
   int sell_sigma;               /* SELL sorting scope sigma; 0 -> 1 (no sorting). 1 or a
                                    multiple of C                                            */
-  unsigned flags;               /* reserved, pass 0                                         */
+  unsigned flags;               /* 0 or KPM_CHECK_HERMITIAN                                 */
 } kpm_options;
+
+/* kpm_options.flags: KPM_CHECK_HERMITIAN makes kpm_set_matrix verify H_ij == conj(H_ji)
+ * (|difference| <= 1e-12 max|H_kl|, duplicates summed, a missing partner counting as 0) over
+ * the entries whose row and column both belong to this rank -- a debug aid, O(nnz log nnz) on
+ * the host; KPM_EINVAL naming the first offending pair otherwise.  The method needs a
+ * Hermitian H (the eta -> mu doubling identities). */
+enum { KPM_CHECK_HERMITIAN = 1u };
 
 typedef struct {
   int64_t n_global;             /* matrix dimension N                               */
@@ -89,8 +96,8 @@ kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt);
 
 /* Store the Hermitian matrix H and the rescaling H~ = a(H - b 1), a > 0.
  * Builds the SELL-C-sigma copy on the device and, for nranks > 1, the
- * halo maps of the row distribution.  Hermiticity is not checked.  Replaces any previous
- * matrix. */
+ * halo maps of the row distribution.  Hermiticity is checked only with
+ * KPM_CHECK_HERMITIAN.  Replaces any previous matrix. */
 kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, double b);
 
 /* Optional locality hint: the order in which the sweep kernels visit the n = n_chunks SELL

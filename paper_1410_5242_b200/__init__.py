@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_PKG, "libkpm.so")
 
 KPM_OK, KPM_EINVAL, KPM_ESTATE, KPM_ERANGE, KPM_ENOMEM, KPM_ECUDA, KPM_ENCCL, KPM_EZERONORM, KPM_WDIVERGED = range(9)
 KPM_MEM_HOST, KPM_MEM_DEVICE = 0, 1
+KPM_CHECK_HERMITIAN = 1
 STATUS_NAMES = ["KPM_OK", "KPM_EINVAL", "KPM_ESTATE", "KPM_ERANGE", "KPM_ENOMEM", "KPM_ECUDA", "KPM_ENCCL",
                 "KPM_EZERONORM", "KPM_WDIVERGED"]
 
@@ -158,11 +159,12 @@ def plan_send(row_begin, row_end, peer, req):
 class KpmContext:
     """One rank's context (kpm_create ... kpm_destroy)."""
 
-    def __init__(self, device=0, nranks=1, rank=0, nccl_unique_id=None, cuda_stream=None, sell_C=32, sell_sigma=1):
+    def __init__(self, device=0, nranks=1, rank=0, nccl_unique_id=None, cuda_stream=None, sell_C=32, sell_sigma=1,
+                 check_hermitian=False):
         self.lib = load_library()
         self._uid = None if nccl_unique_id is None else ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
         opt = kpm_options(device, nranks, rank, ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None,
-                          cuda_stream, sell_C, sell_sigma, 0)
+                          cuda_stream, sell_C, sell_sigma, KPM_CHECK_HERMITIAN if check_hermitian else 0)
         h = ctypes.c_void_p()
         st = self.lib.kpm_create(ctypes.byref(h), ctypes.byref(opt))
         if st != KPM_OK:

@@ -150,6 +150,10 @@ extern "C" kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt) {
     g_create_err = "unsupported SELL parameters (C must be 32, sigma 1 or a multiple of 32)";
     return KPM_EINVAL;
   }
+  if (opt->flags & ~(unsigned)KPM_CHECK_HERMITIAN) {
+    g_create_err = "unknown kpm_options.flags bits";
+    return KPM_EINVAL;
+  }
   kpm_ctx* ctx = new kpm_ctx();
   ctx->opt = *opt;
   ctx->opt.sell_C = C;
@@ -435,6 +439,26 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
       row_begins.push_back(all[3 * q + 1]);
     }
     if (row_begins.back() != H->n_global) return fail(ctx, KPM_EINVAL, "row ranges do not cover n_global");
+  }
+
+  if (ctx->opt.flags & KPM_CHECK_HERMITIAN) {
+    std::vector<int64_t> rp_h, col_h;
+    std::vector<double> val_h;
+    const int64_t *rp = H->row_ptr, *col = H->col;
+    const double* val = H->val;
+    if (H->mem == KPM_MEM_DEVICE) {
+      rp_h.resize(n_loc + 1);
+      KPM_CUDA(cudaMemcpy(rp_h.data(), H->row_ptr, sizeof(int64_t) * (n_loc + 1), cudaMemcpyDeviceToHost));
+      if (rp_h[n_loc] < 0) return fail(ctx, KPM_EINVAL, "malformed row_ptr");
+      col_h.resize(rp_h[n_loc]);
+      val_h.resize(2 * rp_h[n_loc]);
+      KPM_CUDA(cudaMemcpy(col_h.data(), H->col, sizeof(int64_t) * col_h.size(), cudaMemcpyDeviceToHost));
+      KPM_CUDA(cudaMemcpy(val_h.data(), H->val, sizeof(double) * val_h.size(), cudaMemcpyDeviceToHost));
+      rp = rp_h.data(), col = col_h.data(), val = val_h.data();
+    }
+    std::string herr;
+    const int hs = check_hermitian(rp, col, val, n_loc, H->row_begin, H->row_end, H->n_global, 1e-12, herr);
+    if (hs) return fail(ctx, (kpm_status)hs, herr);
   }
 
   reset_sell(ctx->sell);

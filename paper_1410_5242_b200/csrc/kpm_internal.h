@@ -112,6 +112,8 @@ bool variant_wstage(int R, int variant);  // tiled feed: old W staged in shared 
 int variant_stages(int R, int variant);   // tiled feed: preferred ring depth (0 = default)
 cudaError_t launch_aug_spmmv(int R, int variant, bool init, const SweepArgs& a, int grid, cudaStream_t s);
 // kind = KPM_SWEEP_*: the default variant (aug), or it without dots / as a plain SpMMV (main sweep form)
+int check_hermitian(const int64_t* rp, const int64_t* col, const double* val, int64_t n_loc, int64_t row_begin,
+                    int64_t row_end, int64_t n_global, double rtol, std::string& msg);  // hermitian.cpp
 cudaError_t launch_sweep_kind(int R, int kind, const SweepArgs& a, int grid, cudaStream_t s);
 // eta[m][r] (double2) for m in [0, n_sweeps) from partials[m][3R][width] (width = launches x grid)
 cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int width, double2* eta_even,

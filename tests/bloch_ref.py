@@ -46,7 +46,7 @@ def slab_energies(lat, rp, col, val, workers=None):
         return np.concatenate([_row(j) for j in jobs])
     import multiprocessing as mp
 
-    with ProcessPoolExecutor(workers, mp_context=mp.get_context("fork"), initializer=_init_worker) as ex:
+    with ProcessPoolExecutor(workers, mp_context=mp.get_context("spawn"), initializer=_init_worker) as ex:
         return np.concatenate(list(ex.map(_row, jobs, chunksize=max(1, lat.nx // (4 * workers)))))
 
 

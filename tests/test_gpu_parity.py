@@ -412,3 +412,34 @@ def test_c3_full_size_partial_bloch(pkg):
     assert mu[0] == lat.n
     assert np.max(z[1:]) < 6.0, (np.argmax(z), np.max(z))
     assert np.sqrt(np.mean(z[1:] ** 2)) < 1.5
+
+
+def test_check_hermitian_flag(pkg):
+    """KPM_CHECK_HERMITIAN: the TI matrix passes (host and device CSR); a broken conjugate
+    pair or a one-sided entry is rejected with KPM_EINVAL; without the flag it is accepted."""
+    import torch
+
+    lat, rp, col, val, a, b = problem((4, 5, 6))
+    with pkg.KpmContext(check_hermitian=True) as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        d = [torch.from_numpy(x).cuda() for x in (rp, col, val.view(np.float64))]
+        ctx.set_matrix(*d, a, b, mem=pkg.KPM_MEM_DEVICE)
+        mu, _ = ctx.moments(16, 4, SEED)
+        assert mu[0] == lat.n
+        k = int(np.nonzero(col[rp[0]:rp[1]] != 0)[0][0])  # an off-diagonal entry of row 0
+        bad = val.copy()
+        bad[k] += 1e-6j
+        with pytest.raises(pkg.KpmError) as e:
+            ctx.set_matrix(rp, col, bad, a, b)
+        assert e.value.status == pkg.KPM_EINVAL and "not Hermitian" in str(e.value)
+    # row 0 gets an extra entry to column n-1 whose partner is missing
+    rp2 = rp.copy()
+    rp2[1:] += 1
+    col2 = np.insert(col, rp[1], lat.n - 1)
+    val2 = np.insert(val, rp[1], 0.25 + 0j)
+    with pkg.KpmContext(check_hermitian=True) as ctx:
+        with pytest.raises(pkg.KpmError) as e:
+            ctx.set_matrix(rp2, col2, val2, a, b)
+        assert e.value.status == pkg.KPM_EINVAL
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp2, col2, val2, a, b)  # unchecked by default
