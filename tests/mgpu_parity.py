@@ -18,6 +18,22 @@ from workloads.ti_lattice import SEED, Lattice, gershgorin, generate_csr, scale_
 TOL = 1e-10
 
 
+def random_hermitian(n, per_row, seed):
+    """Seeded irregular sparse Hermitian CSR (row lengths vary, columns anywhere)."""
+    rng = np.random.default_rng(seed)
+    i = np.repeat(np.arange(n), rng.integers(1, per_row + 1, size=n))
+    j = rng.integers(0, n, size=i.size)
+    v = rng.normal(size=i.size) + 1j * rng.normal(size=i.size)
+    rows = np.concatenate([i, j, np.arange(n)])
+    cols = np.concatenate([j, i, np.arange(n)])
+    vals = np.concatenate([v, np.conj(v), rng.normal(size=n) + 0j])
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rp, rows + 1, 1)
+    return np.cumsum(rp), cols.astype(np.int64), vals
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -29,31 +45,41 @@ def main():
     dist.broadcast_object_list(uid, src=0)
     results, mu_by_case = {}, {}
     cases = [((8, 8, 8), 64, 4, SEED), ((12, 5, 8), 80, 32, 7), ((10, 3, 5), 40, 5, 11), ((6, 4, 16), 200, 16, 3),
-             ((12, 6, 16), 60, 32, "device")]
+             ((12, 6, 16), 60, 32, "device"), ((max(3, world), 5, 8), 40, 8, 17), ("random", 60, 8, 19)]
     ctx = kpm.KpmContext(device=local, nranks=world, rank=rank, nccl_unique_id=uid[0])
     for (dims, M, R, seed), mode in [(c, m) for m in ("fused", "nccl") for c in cases]:
         os.environ["KPM_HALO"] = mode  # read by kpm_set_matrix
-        lat = Lattice(*dims)
-        planes = [lat.nx * q // world for q in range(world + 1)]
-        rp_g, col_g, val_g = generate_csr(lat)
+        if dims == "random":
+            # irregular Hermitian matrix, uneven row split: every rank exchanges with every
+            # other, halo runs are scattered (not x-planes)
+            n_g = 2900
+            rp_g, col_g, val_g = random_hermitian(n_g, 9, 23)
+            bounds = [0] + [int(n_g * f) for f in np.cumsum(np.arange(1, world + 1) / np.arange(1, world + 1).sum())]
+            bounds[-1] = n_g
+            r0, r1 = bounds[rank], bounds[rank + 1]
+        else:
+            lat = Lattice(*dims)
+            n_g = lat.n
+            planes = [lat.nx * q // world for q in range(world + 1)]
+            rp_g, col_g, val_g = generate_csr(lat)
+            r0, r1 = planes[rank] * lat.rows_per_plane, planes[rank + 1] * lat.rows_per_plane
         a, b = scale_factors(*gershgorin(rp_g, col_g, val_g))
         if seed == "device":  # CSR generated and converted on the GPU (KPM_MEM_DEVICE)
             from workloads.ti_lattice import generate_csr_torch
 
             seed = 13
             rp, col, val = generate_csr_torch(lat, planes[rank], planes[rank + 1], device=f"cuda:{local}")
-            ctx.set_matrix(rp, col, val, a, b, n_global=lat.n, row_begin=planes[rank] * lat.rows_per_plane,
-                           mem=kpm.KPM_MEM_DEVICE)
+            ctx.set_matrix(rp, col, val, a, b, n_global=n_g, row_begin=r0, mem=kpm.KPM_MEM_DEVICE)
         else:
-            rp, col, val = generate_csr(lat, planes[rank], planes[rank + 1])
-            ctx.set_matrix(rp, col, val, a, b, n_global=lat.n, row_begin=planes[rank] * lat.rows_per_plane)
+            rp = rp_g[r0:r1 + 1] - rp_g[r0]
+            col, val = col_g[rp_g[r0]:rp_g[r1]], val_g[rp_g[r0]:rp_g[r1]]
+            ctx.set_matrix(rp, col, val, a, b, n_global=n_g, row_begin=r0)
         mu, eta = ctx.moments(M, R, seed)
         if mode == "fused":
             mu_by_case[dims] = mu
         # explicit v0 path (halo of nu_0 exchanged instead of generated)
         rng = np.random.default_rng(5)
-        v0_g = rng.normal(size=(lat.n, 2)) + 1j * rng.normal(size=(lat.n, 2))
-        r0, r1 = planes[rank] * lat.rows_per_plane, planes[rank + 1] * lat.rows_per_plane
+        v0_g = rng.normal(size=(n_g, 2)) + 1j * rng.normal(size=(n_g, 2))
         mu_v, eta_v = ctx.moments_v0(M, v0_g[r0:r1])
         gathered = [None] * world
         dist.all_gather_object(gathered, (mu.tolist(), mu_v.tolist()))
