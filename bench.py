@@ -152,10 +152,41 @@ def oracle_sample(rp, col, val, a, b, n, nnz, target_s=15.0, max_sweeps=400):
     return gf, threads, sweeps, t
 
 
+def workload(args, world):
+    """Global lattice, per-rank x-slab width, M, R, scaling mode and the config.workload name of
+    a run -- shared by both arms, so the reference line carries this arm's config."""
+    if args.config == "bar":
+        # Bar weak scaling (P:904-905): x grows with the GPU count, each rank owns one C3-sized x-slab
+        px, ny, nz = (int(t) for t in args.lattice.split(","))
+        nx, scaling = px * world, "weak"
+        M, R = args.M or 2000, args.R or 32
+    elif args.config == "C5":
+        px, ny, nz = 1800, 400, 40
+        nx, scaling = px * world, "weak"
+        M, R = args.M or 4000, args.R or 32
+    else:
+        nx, ny, nz = CONFIGS[args.config]["lattice"]
+        px, scaling = nx // world, "strong"
+        if px * world != nx:
+            raise SystemExit(f"{args.config}: Nx={nx} not divisible by {world} ranks")
+        M, R = args.M or CONFIGS[args.config]["M"], args.R or CONFIGS[args.config]["R"]
+    if args.config != "bar":
+        name = f"{args.config} TI lattice {nx}x{ny}x{nz} x 4 orbitals, M={M}, R={R}"
+    elif world == 1:
+        name = f"C3 TI lattice {nx}x{ny}x{nz} x 4 orbitals, M={M}, R={R}"
+    else:
+        name = f"Bar TI lattice {nx}x{ny}x{nz} x 4 orbitals (C3 slab per GPU), M={M}, R={R}"
+    return dict(nx=nx, ny=ny, nz=nz, px=px, M=M, R=R, scaling=scaling, name=name)
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    nx, ny, nz = (200, 100, 40) if args.config == "bar" else CONFIGS[args.config]["lattice"]
+    w = workload(args, world)
+    # bounded sample of the workload: the same lattice structure (rows of the same kind) with at
+    # most ~3.2M rows (x shortened, still periodic), one random vector, a few sweeps per step
+    ny, nz = w["ny"], w["nz"]
+    nx = max(3, min(w["nx"], 3_200_000 // (4 * ny * nz)))
     lat, rp, col, val, a, b = build_problem(nx, ny, nz)
     nnz = int(rp[-1])
     threads = host_cores()
@@ -169,13 +200,14 @@ def run_reference(args, rank, world):
         oracle.kpm_eta(rp, col, val, a, b, 2 * sweeps, 1, SEED, threads=threads)
     t = time.perf_counter() - t0
     value = args.steps * sweeps * alg_flops_per_sweep(lat.n, nnz, 1) / t / 1e9
-    sample = f"lattice {nx}x{ny}x{nz} (N={lat.n}, N_nz={nnz}), 1 random vector, {sweeps} sweeps per step"
+    sample = (f"lattice {nx}x{ny}x{nz} (N={lat.n}, N_nz={nnz}; same row structure), 1 random vector, "
+              f"{sweeps} sweeps per step")
     print(json.dumps({
         "impl": "reference", "metric": "augmented SpMMV Gflop/s (cplx dbl)", "value": value, "unit": "Gflop/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"{'C3' if args.config == 'bar' else args.config} (oracle sample)",
-                   "lattice": [nx, ny, nz], "M": 2 * sweeps, "R": 1},
+        "higher_is_better": True, "scaling": w["scaling"], "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": w["name"], "lattice": [w["nx"], ny, nz], "M": w["M"], "R": w["R"],
+                   "parallelism": f"x-slab dp{world}"},
         "cpu_baseline": {"value": value, "unit": "Gflop/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "Gflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -233,21 +265,8 @@ def main():
         if dist is not None:
             dist.barrier()
 
-    if args.config == "bar":
-        # Bar weak scaling: x grows with the GPU count, each rank owns one C3-sized x-slab
-        px, ny, nz = (int(t) for t in args.lattice.split(","))
-        nx = px * world
-        scaling = "weak"
-    elif args.config == "C5":
-        px, ny, nz = 1800, 400, 40
-        nx = px * world
-        scaling = "weak"
-    else:
-        nx, ny, nz = CONFIGS[args.config]["lattice"]
-        px = nx // world
-        if px * world != nx:
-            raise SystemExit(f"{args.config}: Nx={nx} not divisible by {world} ranks")
-        scaling = "strong"
+    w = workload(args, world)
+    nx, ny, nz, px, scaling, M, R = w["nx"], w["ny"], w["nz"], w["px"], w["scaling"], w["M"], w["R"]
     lat = Lattice(nx, ny, nz)
     x0, x1 = px * rank, px * (rank + 1)
     on_device = args.config == "C5"
@@ -268,12 +287,6 @@ def main():
     lo, hi = -allmax(-lo), allmax(hi)
     a, b = scale_factors(lo, hi)
     n, nnz = lat.n, lat.nnz_expected()
-    if args.config == "bar":
-        M, R = args.M or 2000, args.R or 32
-    elif args.config == "C5":
-        M, R = args.M or 4000, args.R or 32
-    else:
-        M, R = args.M or CONFIGS[args.config]["M"], args.R or CONFIGS[args.config]["R"]
     uid = None
     if world > 1:
         box = [kpm.get_unique_id() if rank == 0 else None]
@@ -338,10 +351,7 @@ def main():
         "metric": "augmented SpMMV Gflop/s (cplx dbl)", "value": value, "unit": "Gflop/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": (f"{args.config} TI lattice {nx}x{ny}x{nz} x 4 orbitals, M={M}, R={R}"
-                                if args.config != "bar" else
-                                f"C3 TI lattice {nx}x{ny}x{nz} x 4 orbitals, M={M}, R={R}" if world == 1 else
-                                f"Bar TI lattice {nx}x{ny}x{nz} x 4 orbitals (C3 slab per GPU), M={M}, R={R}"),
+        "config": {"workload": w["name"],
                    "lattice": [nx, ny, nz], "N": n, "N_nz": nnz, "M": M, "R": R, "parallelism": f"x-slab dp{world}",
                    "hbm_in_use_gb": round((total_b - free_b) / 1e9, 1), "kernel_variant": ctx.last_kernel(), "chunk_order": f"y-band {band}" if band else "storage", "halo": os.environ.get("KPM_HALO", "fused") if world > 1 else None,
                    "l2": ("inputs larger than L2 (V, W %.2f GB each per GPU; matrix %.2f GB)" if
