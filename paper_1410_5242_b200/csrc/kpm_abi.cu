@@ -63,6 +63,7 @@ struct kpm_ctx {
   int64_t* stage_col = nullptr;
   double2* stage_val = nullptr;
   size_t stage_rp_cap = 0, stage_col_cap = 0, stage_val_cap = 0;
+  BuildScratch build_ws;  // device SELL build temporaries
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
@@ -213,6 +214,7 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   cudaFree(ctx->stage_rp);
   cudaFree(ctx->stage_col);
   cudaFree(ctx->stage_val);
+  ctx->build_ws.release();
   if (ctx->h_eta) cudaFreeHost(ctx->h_eta);
   for (int i = 0; i < 4; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
@@ -498,7 +500,7 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
     const bool staged = st_rp != nullptr;
     const int st = build_sell_device(staged ? st_rp : H->row_ptr, staged ? st_col : H->col,
                                      staged ? st_val : reinterpret_cast<const double2*>(H->val), n_loc,
-                                     H->row_begin, H->row_end, H->n_global, d, db, berr, ctx->stream);
+                                     H->row_begin, H->row_end, H->n_global, d, db, ctx->build_ws, berr, ctx->stream);
     if (staged) cudaStreamSynchronize(ctx->stream);
     if (st) {
       reset_sell(ctx->sell);

@@ -130,8 +130,26 @@ struct DeviceBuild {
   std::vector<int64_t> cptr;     // host copy of cptr
   std::vector<char> reads_halo;  // per chunk (empty if no halo)
 };
+// Grow-only device temporaries of build_sell_device, owned by the context (a per-call
+// cudaMalloc/cudaFree of the ~0.3 GB selection buffer cost up to a second per call).
+struct BuildScratch {
+  enum { kFlags, kWidth, kSlots, kTmp, kMaxW, kSel, kNsel, kHalo, kNother, kMaxO, kReadsHalo, kCount };
+  void* p[kCount] = {};
+  size_t cap[kCount] = {};
+  template <class T>
+  cudaError_t get(int i, size_t n, T** out) {
+    const cudaError_t e = reserve(&p[i], &cap[i], n * sizeof(T));
+    *out = static_cast<T*>(p[i]);
+    return e;
+  }
+  void release() {
+    for (int i = 0; i < kCount; ++i) cudaFree(p[i]);
+    *this = BuildScratch();
+  }
+};
 int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val, int64_t n_loc, int64_t row_begin,
-                      int64_t row_end, int64_t n_global, DevSell& d, DeviceBuild& out, std::string& err, cudaStream_t s);
+                      int64_t row_end, int64_t n_global, DevSell& d, DeviceBuild& out, BuildScratch& ws,
+                      std::string& err, cudaStream_t s);
 // Copy records of the tiled feed for block width R from the per-chunk run lists.
 cudaError_t launch_build_records(const int64_t* cptr, const int* nruns, const int* runs, int64_t n_chunks, int R,
                                  int off_w, int off_val, int off_lcol, uint4* rec, cudaStream_t s);

@@ -292,10 +292,11 @@ cudaError_t launch_build_records(const int64_t* cptr, const int* nruns, const in
   } while (0)
 
 int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val, int64_t n_loc, int64_t row_begin,
-                      int64_t row_end, int64_t n_global, DevSell& d, DeviceBuild& out, std::string& err, cudaStream_t s) {
+                      int64_t row_end, int64_t n_global, DevSell& d, DeviceBuild& out, BuildScratch& ws,
+                      std::string& err, cudaStream_t s) {
   out = DeviceBuild();
   int* flags = nullptr;
-  DB_CUDA(cudaMalloc(&flags, sizeof(int)));
+  DB_CUDA(ws.get(BuildScratch::kFlags, 1, &flags));
   DB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), s));
   validate_kernel<<<grid_for(n_loc, 256), 256, 0, s>>>(rp, col, val, n_loc, n_global, flags);
   DB_CUDA(cudaGetLastError());
@@ -306,17 +307,14 @@ int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val,
   DB_CUDA(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
   DB_CUDA(cudaStreamSynchronize(s));
   if (rp0 != 0 || (hflags & 1)) {
-    cudaFree(flags);
     err = "malformed row_ptr";
     return 1;
   }
   if (hflags & 2) {
-    cudaFree(flags);
     err = "column outside [0, n_global)";
     return 3;
   }
   if (hflags & 4) {
-    cudaFree(flags);
     err = "non-finite value";
     return 1;
   }
@@ -327,25 +325,20 @@ int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val,
 
   // chunk widths, cptr
   int64_t *w = nullptr, *slots = nullptr;
-  DB_CUDA(cudaMalloc(&w, sizeof(int64_t) * n_chunks));
-  DB_CUDA(cudaMalloc(&slots, sizeof(int64_t) * n_chunks));
+  DB_CUDA(ws.get(BuildScratch::kWidth, n_chunks, &w));
+  DB_CUDA(ws.get(BuildScratch::kSlots, n_chunks, &slots));
   DB_CUDA(reserve((void**)&d.cptr, &d.cptr_cap, sizeof(int64_t) * (n_chunks + 1)));
   width_kernel<<<grid_for(n_chunks, 256), 256, 0, s>>>(rp, n_loc, n_chunks, w, slots);
   DB_CUDA(cudaGetLastError());
   DB_CUDA(cudaMemsetAsync(d.cptr, 0, sizeof(int64_t), s));
-  void* tmp = nullptr;
-  size_t tmp_bytes = 0, need = 0;
-  auto ensure_tmp = [&](size_t b) -> cudaError_t {
-    if (b <= tmp_bytes) return cudaSuccess;
-    cudaFree(tmp);
-    tmp_bytes = b;
-    return cudaMalloc(&tmp, b);
-  };
+  unsigned char* tmp = nullptr;
+  size_t need = 0;
+  auto ensure_tmp = [&](size_t b) -> cudaError_t { return ws.get(BuildScratch::kTmp, b, &tmp); };
   DB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, need, slots, d.cptr + 1, n_chunks, s));
   DB_CUDA(ensure_tmp(need));
   DB_CUDA(cub::DeviceScan::InclusiveSum(tmp, need, slots, d.cptr + 1, n_chunks, s));
   int64_t* maxw = nullptr;
-  DB_CUDA(cudaMalloc(&maxw, sizeof(int64_t)));
+  DB_CUDA(ws.get(BuildScratch::kMaxW, 1, &maxw));
   DB_CUDA(cub::DeviceReduce::Max(nullptr, need, w, maxw, n_chunks, s));
   DB_CUDA(ensure_tmp(need));
   DB_CUDA(cub::DeviceReduce::Max(tmp, need, w, maxw, n_chunks, s));
@@ -359,8 +352,8 @@ int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val,
   {
     const int64_t piece = std::min<int64_t>(std::max<int64_t>(nnz, 1), (int64_t)1 << 26);
     int64_t *sel = nullptr, *nsel = nullptr;
-    DB_CUDA(cudaMalloc(&sel, sizeof(int64_t) * piece));
-    DB_CUDA(cudaMalloc(&nsel, sizeof(int64_t)));
+    DB_CUDA(ws.get(BuildScratch::kSel, piece, &sel));
+    DB_CUDA(ws.get(BuildScratch::kNsel, 1, &nsel));
     const IsRemote pred{row_begin, row_end};
     std::vector<int64_t> acc;
     for (int64_t b0 = 0; b0 < nnz; b0 += piece) {
@@ -381,10 +374,8 @@ int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val,
     std::sort(acc.begin(), acc.end());
     acc.erase(std::unique(acc.begin(), acc.end()), acc.end());
     out.halo = acc;
-    cudaFree(sel);
-    cudaFree(nsel);
     n_halo = (int64_t)out.halo.size();
-    DB_CUDA(cudaMalloc(&halo, sizeof(int64_t) * std::max<int64_t>(1, n_halo)));
+    DB_CUDA(ws.get(BuildScratch::kHalo, n_halo, &halo));
     if (n_halo) DB_CUDA(cudaMemcpyAsync(halo, out.halo.data(), sizeof(int64_t) * n_halo, cudaMemcpyHostToDevice, s));
   }
   d.n_halo = n_halo;
@@ -406,13 +397,13 @@ int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val,
   DB_CUDA(reserve((void**)&d.nruns, &d.nruns_cap, sizeof(int) * n_chunks));
   DB_CUDA(reserve((void**)&d.runs, &d.runs_cap, sizeof(int) * 2 * kMaxRuns * n_chunks));
   int* nother = nullptr;
-  DB_CUDA(cudaMalloc(&nother, sizeof(int) * n_chunks));
+  DB_CUDA(ws.get(BuildScratch::kNother, n_chunks, &nother));
   DB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), s));
   tiles_kernel<<<(int)std::min<int64_t>(n_chunks, 148 * 16), 256, 0, s>>>(d.col, d.cptr, n_chunks, d.lcol, d.nruns,
                                                                           d.runs, nother, flags);
   DB_CUDA(cudaGetLastError());
   int* maxo = nullptr;
-  DB_CUDA(cudaMalloc(&maxo, sizeof(int)));
+  DB_CUDA(ws.get(BuildScratch::kMaxO, 1, &maxo));
   DB_CUDA(cub::DeviceReduce::Max(nullptr, need, nother, maxo, n_chunks, s));
   DB_CUDA(ensure_tmp(need));
   DB_CUDA(cub::DeviceReduce::Max(tmp, need, nother, maxo, n_chunks, s));
@@ -424,25 +415,16 @@ int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val,
   DB_CUDA(cudaMemcpyAsync(out.cptr.data(), d.cptr, sizeof(int64_t) * (n_chunks + 1), cudaMemcpyDeviceToHost, s));
   if (n_halo) {
     char* rh = nullptr;
-    DB_CUDA(cudaMalloc(&rh, n_chunks));
+    DB_CUDA(ws.get(BuildScratch::kReadsHalo, n_chunks, &rh));
     reads_halo_kernel<<<grid_for(n_chunks * 32, 256), 256, 0, s>>>(d.col, d.cptr, n_chunks, n_pad, rh);
     DB_CUDA(cudaGetLastError());
     out.reads_halo.resize(n_chunks);
     DB_CUDA(cudaMemcpyAsync(out.reads_halo.data(), rh, n_chunks, cudaMemcpyDeviceToHost, s));
     DB_CUDA(cudaStreamSynchronize(s));
-    cudaFree(rh);
   }
   DB_CUDA(cudaStreamSynchronize(s));
   d.max_other = hmaxo;
   d.tiles_ok = (hflags & (8 | 16)) == 0;
-  cudaFree(w);
-  cudaFree(slots);
-  cudaFree(maxw);
-  cudaFree(maxo);
-  cudaFree(nother);
-  cudaFree(halo);
-  cudaFree(tmp);
-  cudaFree(flags);
   return 0;
 }
 

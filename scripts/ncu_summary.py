@@ -71,7 +71,8 @@ def main():
         print("\n".join(lines))
     traffic_path = os.path.join(prof, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
-    summary = {}
+    full_path = os.path.join(prof, f"{args.round}_ncu_full.json")
+    summary = json.load(open(full_path)) if os.path.exists(full_path) else {}  # merge: captures come per call
     for spec in args.full:
         rep, tag = spec.split(":")
         d = raw(rep)
@@ -92,7 +93,7 @@ def main():
         traffic[f"{lattice}/{r}/smem_wavefronts"] = smem
     if args.full:
         json.dump(traffic, open(traffic_path, "w"), indent=1, sort_keys=True)
-        with open(os.path.join(prof, f"{args.round}_ncu_full.json"), "w") as f:
+        with open(full_path, "w") as f:
             json.dump(summary, f, indent=1)
         print(json.dumps(summary, indent=1))
 
