@@ -13,6 +13,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+from oracle import sell_ref  # noqa: E402
 from workloads.ti_lattice import SEED, Lattice, gershgorin, generate_csr, scale_factors  # noqa: E402
 
 TOL = 1e-10
@@ -74,6 +75,14 @@ def main():
             rp = rp_g[r0:r1 + 1] - rp_g[r0]
             col, val = col_g[rp_g[r0]:rp_g[r1]], val_g[rp_g[r0]:rp_g[r1]]
             ctx.set_matrix(rp, col, val, a, b, n_global=n_g, row_begin=r0)
+        # the rank's SELL copy and halo map, bit-exact against the numpy reference builder
+        bounds_all = np.array(bounds if dims == "random" else [q * lat.rows_per_plane for q in planes], dtype=np.int64)
+        ref = sell_ref.build_sell(rp_g[r0:r1 + 1] - rp_g[r0], col_g[rp_g[r0]:rp_g[r1]], val_g[rp_g[r0]:rp_g[r1]],
+                                  row_begin=r0, row_end=r1, row_begins=bounds_all)
+        ex = ctx.export_sell()
+        sell_ok = all(np.array_equal(ex[k], ref[k]) for k in ("cptr", "col", "val", "perm", "halo"))
+        sell_all = [None] * world
+        dist.all_gather_object(sell_all, bool(sell_ok))
         mu, eta = ctx.moments(M, R, seed)
         if mode == "fused":
             mu_by_case[dims] = mu
@@ -95,7 +104,9 @@ def main():
             v_err = float(np.max(np.abs(eta_v - eta_vo) / eta_vo[:, :1].real))
             same = all(np.array_equal(np.array(g[0]), mu) for g in gathered)
             results[f"{dims}/{mode}"] = dict(col_err=col_err, mu_err=mu_err, v0_err=v_err, ranks_identical=bool(same),
-                                      ok=bool(col_err <= TOL and mu_err <= TOL and v_err <= TOL and same))
+                                             sell_halo_exact=all(sell_all),
+                                             ok=bool(col_err <= TOL and mu_err <= TOL and v_err <= TOL and same
+                                                     and all(sell_all)))
     ctx.close()
     if rank == 0:
         # P-invariance against a single-rank context on the same device
