@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--R", default="1,2,4,8,16,32")
     ap.add_argument("--M", type=int, default=40)
     ap.add_argument("--grid-per-sm", default="0")
+    ap.add_argument("--variants", default="", help="comma list of variant indices (default: all)")
     ap.add_argument("--warm-seconds", type=float, default=0.0, help="run this long before timing (power-cap steady state)")
     args = ap.parse_args()
     import paper_1410_5242_b200 as kpm
@@ -29,7 +30,8 @@ def main():
     for R in (int(r) for r in args.R.split(",")):
         ref = None
         names = set()
-        for v in range(8):
+        vlist = [int(x) for x in args.variants.split(",")] if args.variants else range(16)
+        for v in vlist:
             for g in args.grid_per_sm.split(","):
                 os.environ["KPM_VARIANT"] = str(v)
                 os.environ["KPM_GRID_PER_SM"] = g
@@ -43,7 +45,7 @@ def main():
                     mu, _ = ctx.moments(args.M, R, SEED, want_eta=False)
                     name = ctx.last_kernel()
                     t, sw, ns = ctx.last_timing()
-                if v > 0 and name in names and g == args.grid_per_sm.split(",")[0]:
+                if not args.variants and v > 0 and name in names and g == args.grid_per_sm.split(",")[0]:
                     break
                 names.add(name)
                 if ref is None:
