@@ -81,7 +81,8 @@ typedef struct {
   int64_t row_begin, row_end;   /* this rank's rows [row_begin, row_end)                    */
   const int64_t* row_ptr;       /* row_end-row_begin+1 entries, row_ptr[0] == 0, non-decreasing */
   const int64_t* col;           /* row_ptr[last] global column ids, in [0, n_global); any
-                                   order inside a row (that order is the summation order)   */
+                                   order inside a row (the summation order: the row's
+                                   diagonal entry, if stored, first, then this order)       */
   const double* val;            /* 2*row_ptr[last] doubles, interleaved (re, im)            */
   int mem;                      /* KPM_MEM_HOST or KPM_MEM_DEVICE (all three arrays)        */
 } kpm_csr;

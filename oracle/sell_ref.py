@@ -12,7 +12,8 @@ Layout contract:
   * chunk c holds positions [c*C, (c+1)*C); clen[c] = max length of its rows (0 for
     padding positions p >= n_loc); cptr[c] = sum_{c' < c} C * clen[c'] (int64).
   * entry j of the row at position p = c*C + k lives at cptr[c] + j*C + k (column-major
-    inside the chunk); within-row entry order is the CSR order.
+    inside the chunk); within-row entry order: the row's own-position (diagonal) entry
+    first, if stored (first occurrence), then the other entries in CSR order.
   * columns are renumbered: a local column i becomes invperm[i]; a column owned by
     another rank becomes n_pad + h, n_pad = n_chunks*C, h = its slot in the halo list.
   * padding slots: value 0 + 0i, column = p (the slot's own position).
@@ -82,10 +83,18 @@ def build_sell(row_ptr, col, val, C=32, sigma=1, row_begin=0, row_end=None, row_
     new_col[local] = invperm[col[local] - row_begin]
     new_col[~local] = n_pad + np.searchsorted(halo, col[~local])
 
-    # scatter entries: row i at position p = invperm[i], entry j -> cptr[p//C] + j*C + p%C
+    # scatter entries: row i at position p = invperm[i], entry j -> cptr[p//C] + j*C + p%C.
+    # Entry order within a row: the row's own-position (diagonal) entry first, if stored
+    # (its first occurrence), then the other entries in stored order (R18).
     rows = np.repeat(np.arange(n_loc), lens)
     j = np.arange(len(col)) - np.repeat(row_ptr[:-1], lens)
     p = invperm[rows]
+    is_diag = new_col == p
+    jd = np.full(n_loc, np.iinfo(np.int64).max, dtype=np.int64)
+    np.minimum.at(jd, rows[is_diag], j[is_diag])
+    jd_e = jd[rows]
+    has_d = jd_e != np.iinfo(np.int64).max
+    j = np.where(has_d & (j == jd_e), 0, np.where(has_d & (j < jd_e), j + 1, j))
     dest = cptr[p // C] + j * C + p % C
     s_val[dest] = val
     s_col[dest] = new_col

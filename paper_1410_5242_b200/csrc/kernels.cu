@@ -444,8 +444,10 @@ __host__ __device__ constexpr int tiled_threads() { return 32 * (tiled_ncwg<LPR>
 //   kAug       the fully augmented SpMMV of Fig. 5 (the hot path),
 //   kAugNoDot  the same without the on-the-fly dot products,
 //   kSpmmv     the plain SpMMV W = H V (no shift/scale, no old W).
-template <int R, int LPR, int U, int CS, bool WS, bool INIT, int KIND = kAug>
-__global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(const SweepArgs a) {
+// MINB: CTAs per SM the register allocation must leave room for (2 for the variants whose
+// smaller ring is meant to fit two CTAs per SM).
+template <int R, int LPR, int U, int CS, bool WS, bool INIT, int KIND = kAug, int MINB = 1>
+__global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tiled(const SweepArgs a) {
   using Cf = Cfg<R, LPR, U>;
   constexpr int RW = Cf::RW, G = kC / RW;
   static_assert(Cf::CPL % CS == 0, "column split must divide the columns per lane");
@@ -553,6 +555,25 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
         const uint16_t* sl = slc + kr;
         const double2* sVt = sV + t;
         int j = 0;
+        // The SELL order puts a row's own-position (diagonal) entry first, if stored (DESIGN.md
+        // R18): then entry 0's gather is the own row V_i, which the epilogue needs as well, so
+        // it is kept in registers instead of being read from shared memory a second time.
+        // (Only without a multi-CTA register cap: there x0's live range costs more than the
+        // saved read, measured at R = 8 and 16.)
+        constexpr bool PEEL = MINB == 1;
+        double2 x0[CPL];
+        int li0 = -1;
+        if (PEEL && L > 0) {  // uniform per tile
+          const double2 h0 = sv[0];
+          li0 = sl[0] * R;
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) {
+            x0[cc] = sVt[li0 + (cc ^ sw) * LPR];
+            cmac(u[cc], h0, x0[cc]);
+          }
+          j = 1;
+        }
+        const bool own0 = PEEL && li0 == kr * R;
         for (; j + U <= L; j += U) {  // full batches: no predication
           double2 h[U];
           int li[U];
@@ -585,10 +606,10 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
               st_stream(a.W + p * R + col, u[cc], pol);
               continue;
             }
-            const double2 vi = sV[kr * R + col];
+            const double2 vi_c = own0 ? x0[cc] : sV[kr * R + col];
             double2 uu = u[cc];
-            uu.x = fma(-a.b, vi.x, uu.x);
-            uu.y = fma(-a.b, vi.y, uu.y);
+            uu.x = fma(-a.b, vi_c.x, uu.x);
+            uu.y = fma(-a.b, vi_c.y, uu.y);
             double2 w;
             if (INIT) {
               w = make_double2(a.scale * uu.x, a.scale * uu.y);
@@ -599,9 +620,9 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
             st_stream(a.W + p * R + col, w, pol);
             store_peers<R>(a, p, col, w);
             if (KIND == kAug) {
-              d.ee[cc] = fma(vi.x, vi.x, fma(vi.y, vi.y, d.ee[cc]));
-              d.eor[cc] = fma(w.x, vi.x, fma(w.y, vi.y, d.eor[cc]));
-              d.eoi[cc] = fma(w.x, vi.y, fma(-w.y, vi.x, d.eoi[cc]));
+              d.ee[cc] = fma(vi_c.x, vi_c.x, fma(vi_c.y, vi_c.y, d.ee[cc]));
+              d.eor[cc] = fma(w.x, vi_c.x, fma(w.y, vi_c.y, d.eor[cc]));
+              d.eoi[cc] = fma(w.x, vi_c.y, fma(-w.y, vi_c.x, d.eoi[cc]));
             }
           }
         }
@@ -654,7 +675,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), 1) aug_spmmv_tiled(c
 
 enum Feed { kDirect = 0, kStaged = 1, kTiled = 2 };
 
-template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true>
+template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true, int MINB = 1>
 struct Variant {
   static cudaError_t launch(bool init, const SweepArgs& a, int grid, cudaStream_t s) {
     if constexpr (FEED == kStaged) {
@@ -664,12 +685,11 @@ struct Variant {
         aug_spmmv_staged<R, LPR, U, false><<<grid, kThreads, kStagedSmem, s>>>(a);
     } else if constexpr (FEED == kTiled) {
       const int smem = a.tl.stages * a.tl.stage_bytes;
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (init)
-        aug_spmmv_tiled<R, LPR, U, CS, WS, true><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
-      else
-        aug_spmmv_tiled<R, LPR, U, CS, WS, false><<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
+      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB>;
+      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB>;
+      cudaFuncSetAttribute(k_init, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      (init ? k_init : k_main)<<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
     } else {
       if (init)
         aug_spmmv_direct<R, LPR, U, true><<<grid, kThreads, 0, s>>>(a);
@@ -683,9 +703,9 @@ struct Variant {
     if constexpr (FEED == kStaged) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_staged<R, LPR, U, false>, kThreads, kStagedSmem);
     } else if constexpr (FEED == kTiled) {
-      cudaFuncSetAttribute(aug_spmmv_tiled<R, LPR, U, CS, WS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_tiled<R, LPR, U, CS, WS, false>, tiled_threads<LPR, CS>(),
-                                                    dyn_smem);
+      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB>;
+      cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_main, tiled_threads<LPR, CS>(), dyn_smem);
     } else {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_direct<R, LPR, U, false>, kThreads, 0);
     }
@@ -707,9 +727,11 @@ struct Entry {
 #define KPM_VARIANT(R, LPR, U, F, NAME) {R, NAME, F, true, Variant<R, LPR, U, F>::launch, Variant<R, LPR, U, F>::occupancy}
 #define KPM_VARIANT_CS(R, LPR, U, CS, NAME) \
   {R, NAME, kTiled, true, Variant<R, LPR, U, kTiled, CS>::launch, Variant<R, LPR, U, kTiled, CS>::occupancy}
-#define KPM_VARIANT_WR_S(R, LPR, U, S, NAME)                                                             \
-  {R, NAME, kTiled, false, Variant<R, LPR, U, kTiled, 1, false>::launch, Variant<R, LPR, U, kTiled, 1, false>::occupancy, \
-   S}
+// S-deep ring, W via registers; registers capped so that the CTAs the smaller ring is meant
+// for fit per SM (3 for R <= 8, 2 above)
+#define KPM_VARIANT_WR_S(R, LPR, U, S, NAME)                                                                 \
+  {R, NAME, kTiled, false, Variant<R, LPR, U, kTiled, 1, false, (R <= 8 ? 3 : 2)>::launch,                     \
+   Variant<R, LPR, U, kTiled, 1, false, (R <= 8 ? 3 : 2)>::occupancy, S}
 #define KPM_VARIANT_WR(R, LPR, U, NAME) \
   {R, NAME, kTiled, false, Variant<R, LPR, U, kTiled, 1, false>::launch, Variant<R, LPR, U, kTiled, 1, false>::occupancy}
 // First entry of each width is the default (chosen from the B200 measurements in DESIGN.md).

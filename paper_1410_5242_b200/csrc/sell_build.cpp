@@ -99,10 +99,19 @@ int build_sell_host(const int64_t* row_ptr, const int64_t* col, const double* va
       const int64_t p = c * C + k;
       const int64_t nrow = (p < n_loc) ? len[out.perm[p]] : 0;
       const int64_t src = (p < n_loc) ? row_ptr[out.perm[p]] : 0;
+      // own-position (diagonal) entry first, then the others in stored order (R18)
+      const int64_t gdiag = row_begin + ((p < n_loc) ? (int64_t)out.perm[p] : 0);
+      int64_t jd = nrow;
+      for (int64_t j = 0; j < nrow; ++j)
+        if (col[src + j] == gdiag) {
+          jd = j;
+          break;
+        }
       for (int64_t j = 0; j < L; ++j) {
         const int64_t d = out.cptr[c] + j * C + k;
         if (j < nrow) {
-          const int64_t g = col[src + j];
+          const int64_t js = jd == nrow ? j : (j == 0 ? jd : (j <= jd ? j - 1 : j));  // source entry
+          const int64_t g = col[src + js];
           int64_t lc;
           if (g >= row_begin && g < row_end) {
             lc = invperm[g - row_begin];
@@ -110,8 +119,8 @@ int build_sell_host(const int64_t* row_ptr, const int64_t* col, const double* va
             lc = out.n_pad + (std::lower_bound(halo.begin(), halo.end(), g) - halo.begin());
           }
           out.col[d] = (int32_t)lc;
-          out.val[2 * d] = val[2 * (src + j)];
-          out.val[2 * d + 1] = val[2 * (src + j) + 1];
+          out.val[2 * d] = val[2 * (src + js)];
+          out.val[2 * d + 1] = val[2 * (src + js) + 1];
         } else {
           out.col[d] = (int32_t)p;  // padding: value 0, column = own position
           out.val[2 * d] = 0.0;

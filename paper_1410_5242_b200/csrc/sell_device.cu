@@ -75,12 +75,20 @@ __global__ void scatter_kernel(const int64_t* __restrict__ rp, const int64_t* __
     const int64_t p = c * kC + lane;
     const int64_t base = p < n_loc ? rp[p] : 0;
     const int len = p < n_loc ? (int)(rp[p + 1] - base) : 0;
+    // own-position (diagonal) entry first, then the others in stored order (R18)
+    int jd = len;
+    for (int j = 0; j < len; ++j)
+      if (col[base + j] == row_begin + p) {
+        jd = j;
+        break;
+      }
     for (int j = 0; j < L; ++j) {
       const int64_t d = s0 + (int64_t)j * kC + lane;
       if (j < len) {
-        const int64_t g = col[base + j];
+        const int js = jd == len ? j : (j == 0 ? jd : (j <= jd ? j - 1 : j));  // source entry
+        const int64_t g = col[base + js];
         scol[d] = (int)(g >= row_begin && g < row_end ? g - row_begin : n_pad + lower_bound_i64(halo, n_halo, g));
-        sval[d] = val[base + j];
+        sval[d] = val[base + js];
       } else {
         scol[d] = (int)p;
         sval[d] = make_double2(0.0, 0.0);

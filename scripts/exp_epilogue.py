@@ -68,7 +68,7 @@ def main():
     lat = Lattice(200, 100, 40)
     rp, col, val = generate_csr(lat)
     a, b = scale_factors(*gershgorin(rp, col, val))
-    for R in (16, 32):
+    for R in [int(r) for r in os.environ.get("EXP_R", "8,16,32").split(",")]:
         with kpm.KpmContext() as ctx:
             ctx.set_matrix(rp, col, val, a, b)
             ctx.moments(200, R, SEED, want_eta=False)
@@ -76,7 +76,7 @@ def main():
             for _ in range(3):
                 ctx.moments(400, R, SEED, want_eta=False)
                 best = min(best, ctx.last_timing()[1])
-            print(json.dumps(dict(exp=int(e), R=R, kernel=ctx.last_kernel(), sweep_ms=best)), flush=True)
+            print(json.dumps(dict(exp=e, R=R, kernel=ctx.last_kernel(), sweep_ms=best)), flush=True)
 
 
 if __name__ == "__main__":

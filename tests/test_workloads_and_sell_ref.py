@@ -67,13 +67,33 @@ def test_bloch_spectrum_and_gershgorin():
 
 
 # ------------------------------------------------------------------ SELL reference ----
+def _diag_first(rp, col, val):
+    """CRS rows with each row's diagonal entry moved to the front (R18)."""
+    oc, ov = [], []
+    for i in range(len(rp) - 1):
+        c, v = list(col[rp[i] : rp[i + 1]]), list(val[rp[i] : rp[i + 1]])
+        if i in c:
+            k = c.index(i)
+            c = [c[k]] + c[:k] + c[k + 1 :]
+            v = [v[k]] + v[:k] + v[k + 1 :]
+        oc += c
+        ov += v
+    return np.array(oc), np.array(ov)
+
+
 def test_sell1_is_crs():
-    """C=1, sigma=1 -> the CRS value sequence."""
+    """C=1, sigma=1 -> the CRS sequence, each row's diagonal first."""
     lat = Lattice(3, 3, 3)
     rp, col, val = generate_csr(lat)
     s = sell_ref.build_sell(rp, col, val, C=1, sigma=1)
-    assert np.array_equal(s["val"], val)
-    assert np.array_equal(s["col"], col.astype(np.int32))
+    ec, ev = _diag_first(rp, col, val)
+    assert np.array_equal(s["val"], ev)
+    assert np.array_equal(s["col"], ec.astype(np.int32))
+    assert not np.array_equal(ec, col)  # the TI's diagonal is not first in CRS order
+    # a row without a stored diagonal keeps its order
+    rp2, col2, val2 = np.array([0, 2, 3]), np.array([1, 0, 0]), np.array([1 + 1j, 2, 3])
+    s2 = sell_ref.build_sell(rp2, col2, val2, C=1, sigma=1)
+    assert list(s2["col"]) == [0, 1, 0] and list(s2["val"]) == [2, 1 + 1j, 3]
 
 
 @pytest.mark.parametrize("C,sigma", [(32, 1), (32, 64), (4, 8), (32, 128)])
@@ -91,11 +111,12 @@ def test_sell_round_trip_and_spmv(C, sigma):
     ref = sorted(zip(invperm[rows].tolist(), invperm[col].tolist(), val.tolist()))
     got = sorted((p, c, v) for p, c, v in ent if v != 0)
     assert got == ref
-    # within-row order preserved
+    # within-row order: the diagonal first, then the stored order
+    _, ev = _diag_first(rp, col, val)
     p0 = invperm[7]
     c0 = p0 // C
     js = [int(s["cptr"][c0]) + j * C + p0 % C for j in range(rp[8] - rp[7])]
-    assert np.array_equal(s["val"][js], val[rp[7] : rp[8]])
+    assert np.array_equal(s["val"][js], ev[rp[7] : rp[8]])
     # SpMV in permuted numbering
     x = np.random.default_rng(0).normal(size=n) + 1j * np.random.default_rng(1).normal(size=n)
     xp = np.zeros(s["n_pad"], dtype=np.complex128)
