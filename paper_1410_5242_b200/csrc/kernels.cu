@@ -559,11 +559,12 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
         // R18): then entry 0's gather is the own row V_i, which the epilogue needs as well, so
         // it is kept in registers instead of being read from shared memory a second time.
         // (Only without a multi-CTA register cap: there x0's live range costs more than the
-        // saved read, measured at R = 8 and 16.)
+        // saved read, measured at R = 8 and 16; entry 0 is still peeled, keeping the batches
+        // of the TI's 13-entry rows full.)
         constexpr bool PEEL = MINB == 1;
         double2 x0[CPL];
         int li0 = -1;
-        if (PEEL && L > 0) {  // uniform per tile
+        if (L > 0) {  // uniform per tile
           const double2 h0 = sv[0];
           li0 = sl[0] * R;
 #pragma unroll
