@@ -284,6 +284,56 @@ def test_device_build_errors(pkg):
         assert ei.value.status == pkg.KPM_ERANGE
 
 
+def _rows_without_diagonal():
+    """TI lattice (10x9x16) whose diagonal entry is dropped in every third row (H_ii = 0 not
+    stored) and split into two entries in every seventh row: the diagonal-first SELL order
+    (R18) then meets rows where entry 0 is not the own row, rows where it is, and
+    duplicates, inside the same warps of the tiled kernel."""
+    lat = Lattice(10, 9, 16)
+    rp, col, val = generate_csr(lat)
+    rows, cols, vals = [], [], []
+    for i in range(lat.n):
+        c, v = col[rp[i] : rp[i + 1]], val[rp[i] : rp[i + 1]]
+        for cj, vj in zip(c, v):
+            if cj == i and i % 3 == 0:
+                continue
+            if cj == i and i % 7 == 0:
+                rows += [i, i]
+                cols += [cj, cj]
+                vals += [0.25 * vj, 0.75 * vj]
+                continue
+            rows.append(i)
+            cols.append(cj)
+            vals.append(vj)
+    rows = np.array(rows)
+    rp2 = np.zeros(lat.n + 1, dtype=np.int64)
+    np.add.at(rp2, rows + 1, 1)
+    return lat, np.cumsum(rp2), np.array(cols, dtype=np.int64), np.array(vals, dtype=np.complex128)
+
+
+@pytest.mark.parametrize("R", [2, 8, 16, 32])
+def test_rows_without_diagonal(pkg, R):
+    lat, rp, col, val = _rows_without_diagonal()
+    a, b = scale_factors(*gershgorin(rp, col, val))
+    import torch
+
+    M = 64
+    eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, SEED)
+    ref = sell_ref.build_sell(rp, col, val)
+    for dev in (False, True):  # host builder, device builder
+        with pkg.KpmContext() as ctx:
+            if dev:
+                ctx.set_matrix(torch.as_tensor(rp, device="cuda"), torch.as_tensor(col, device="cuda"),
+                               torch.as_tensor(val, device="cuda"), a, b, n_global=lat.n, mem=pkg.KPM_MEM_DEVICE)
+            else:
+                ctx.set_matrix(rp, col, val, a, b)
+            mu, eta = ctx.moments(M, R, SEED)
+            assert ctx.last_kernel().startswith("tiled")
+            s = ctx.export_sell()
+        check(eta, mu, eta_o)
+        assert np.array_equal(s["col"], ref["col"]) and np.array_equal(s["val"], ref["val"])
+
+
 @pytest.mark.parametrize("R", [1, 8, 32])
 def test_irregular_matrix_fallback(pkg, R):
     """A random Hermitian matrix with empty rows, wide rows (up to ~200 entries) and scattered
