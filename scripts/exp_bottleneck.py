@@ -28,7 +28,7 @@ def build_libs():
     shutil.copytree(os.path.join(root, "include"), os.path.join(tmp, "include"))
     subprocess.run(["patch", "-p1", "-i", os.path.join(root, "scripts", "exp_bottleneck.patch")], cwd=tmp, check=True)
     nccl = b._nccl_dir()
-    for e in range(4):
+    for e in [int(x) for x in os.environ.get("EXP_LIST", "0,1,2,3").split(",")]:
         cmd = [b._nvcc(), *b.GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
                f"-DKPM_EXP={e}", f"-I{os.path.join(root, 'include')}", f"-I{nccl}/include",
                "-o", os.path.join(root, "exp", f"libkpm_e{e}.so")]
