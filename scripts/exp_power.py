@@ -33,7 +33,7 @@ def main():
                                 "-i", "0", "-lms", "100"], stdout=subprocess.PIPE, text=True)
         sweeps = []
         for _ in range(4):
-            ctx.moments(2000, R, SEED, want_eta=False)
+            mu, _ = ctx.moments(2000, R, SEED, want_eta=False, allow_warning=True)
             sweeps.append(ctx.last_timing()[1])
         smi.terminate()
         out = smi.communicate()[0]
@@ -49,7 +49,7 @@ def main():
     mhz.sort()
     print(json.dumps(dict(exp=int(e), R=R, sweep_ms=sorted(sweeps)[len(sweeps) // 2],
                           power_w=pw[len(pw) // 2] if pw else None, sm_mhz=mhz[len(mhz) // 2] if mhz else None,
-                          samples=len(pw))), flush=True)
+                          samples=len(pw), mu2=float(mu[2]), mu_last=float(mu[-1]))), flush=True)
 
 
 if __name__ == "__main__":
