@@ -163,6 +163,10 @@ kpm_status kpm_last_timing(const kpm_ctx* ctx, double* total_ms, double* sweep_m
  * width for tuning; the default is variant 0. */
 const char* kpm_last_kernel(const kpm_ctx* ctx);
 
+/* Name of kernel variant `variant` (the KPM_VARIANT index) of block width R (1, 2, 4, ..., 32),
+ * NULL if there is none; host-only, needs no GPU.  Variant 0 is the width's default. */
+const char* kpm_variant_name(int R, int variant);
+
 /* Sizes of the SELL copy, for kpm_export_sell.  n_chunks*C = n_pad. */
 typedef struct {
   int64_t n_loc;     /* local rows                                       */

@@ -23,7 +23,7 @@ STATUS_NAMES = ["KPM_OK", "KPM_EINVAL", "KPM_ESTATE", "KPM_ERANGE", "KPM_ENOMEM"
 # exported symbols declared in include/kpm.h
 ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_dos", "kpm_export_sell", "kpm_get_sell_info", "kpm_get_unique_id",
                "kpm_last_error", "kpm_last_kernel", "kpm_last_timing", "kpm_moments", "kpm_moments_stage", "kpm_moments_v0",
-               "kpm_plan_recv", "kpm_plan_send", "kpm_set_chunk_order", "kpm_set_matrix", "kpm_sweep_kernel"]
+               "kpm_plan_recv", "kpm_plan_send", "kpm_set_chunk_order", "kpm_set_matrix", "kpm_sweep_kernel", "kpm_variant_name"]
 
 
 class KpmError(RuntimeError):
@@ -75,6 +75,8 @@ def load_library():
     lib.kpm_last_error.restype = ctypes.c_char_p
     lib.kpm_last_kernel.argtypes = [P]
     lib.kpm_last_kernel.restype = ctypes.c_char_p
+    lib.kpm_variant_name.argtypes = [i32, i32]
+    lib.kpm_variant_name.restype = ctypes.c_char_p
     lib.kpm_get_unique_id.argtypes = [P]
     lib.kpm_set_chunk_order.argtypes = [P, P, i64]
     lib.kpm_dos.argtypes = [i32, P, dbl, dbl, i32, P, i32, P, P]
@@ -83,7 +85,7 @@ def load_library():
     lib.kpm_destroy.argtypes = [P]
     lib.kpm_destroy.restype = None
     for name in ABI_SYMBOLS:
-        if name not in ("kpm_last_error", "kpm_last_kernel", "kpm_destroy"):
+        if name not in ("kpm_last_error", "kpm_last_kernel", "kpm_destroy", "kpm_variant_name"):
             getattr(lib, name).restype = i32
     _lib = lib
     return lib
@@ -95,6 +97,12 @@ def _ptr(a):
     if isinstance(a, np.ndarray):
         return a.ctypes.data_as(ctypes.c_void_p)
     return ctypes.c_void_p(int(a.data_ptr()))  # torch tensor (device memory plumbing)
+
+
+def variant_name(R, variant):
+    """kpm_variant_name: name of kernel variant `variant` (KPM_VARIANT index) of width R, or None."""
+    n = load_library().kpm_variant_name(int(R), int(variant))
+    return n.decode() if n else None
 
 
 def get_unique_id() -> bytes:

@@ -446,7 +446,10 @@ __host__ __device__ constexpr int tiled_threads() { return 32 * (tiled_ncwg<LPR>
 //   kSpmmv     the plain SpMMV W = H V (no shift/scale, no old W).
 // MINB: CTAs per SM the register allocation must leave room for (2 for the variants whose
 // smaller ring is meant to fit two CTAs per SM).
-template <int R, int LPR, int U, int CS, bool WS, bool INIT, int KIND = kAug, int MINB = 1>
+// BC: block-cache feed: records per list position, V rows of a tile live in a
+// pool of 32-row blocks kept across the CTA's tiles (plus per-stage extra rows), lcol holds
+// absolute shared-memory V rows, the header carries the own block's first row.
+template <int R, int LPR, int U, int CS, bool WS, bool INIT, int KIND = kAug, int MINB = 1, bool BC = false>
 __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tiled(const SweepArgs a) {
   using Cf = Cfg<R, LPR, U>;
   constexpr int RW = Cf::RW, G = kC / RW;
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
   constexpr bool W_TILE = NEED_W && WS;             // old W rows staged in the tile
   extern __shared__ __align__(128) unsigned char tsm[];
   __shared__ __align__(8) uint64_t full[kMaxTileStages], empty[kMaxTileStages];
-  __shared__ int tile_len[kMaxTileStages];
+  __shared__ int tile_len[kMaxTileStages], tile_own[kMaxTileStages];
   __shared__ int64_t tile_chunk[kMaxTileStages];
   __shared__ double red[NCWG * 3 * R];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -486,23 +489,27 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
     // the producer's critical path.
     const uint64_t pol_v = a.v_evict_last ? policy_evict_last() : 0ull;
     int64_t c_nxt = my_tiles > 0 ? chunk_at(a, blockIdx.x) : 0;
-    uint4 nxt = my_tiles > 0 && lane < 16 ? __ldg(a.rec + c_nxt * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
+    uint4 nxt = my_tiles > 0 && lane < 16 ? __ldg(a.rec + (BC ? (int64_t)blockIdx.x : c_nxt) * 16 + lane)
+                                          : make_uint4(0u, 0u, 0u, 0u);
     for (int64_t k = 0; k < my_tiles; ++k) {
       const uint4 cur = nxt;
       const int64_t c_cur = c_nxt;
       if (k + 1 < my_tiles) {
         c_nxt = chunk_at(a, blockIdx.x + (k + 1) * gridDim.x);
-        nxt = lane < 16 ? __ldg(a.rec + c_nxt * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
+        const int64_t ri = BC ? blockIdx.x + (k + 1) * gridDim.x : c_nxt;
+        nxt = lane < 16 ? __ldg(a.rec + ri * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
       }
       const int s = (int)(k % tl.stages);
       const uint32_t total = __shfl_sync(0xffffffffu, W_TILE ? cur.x : cur.y, 0);
       const uint32_t L = __shfl_sync(0xffffffffu, cur.z, 0);
-      const uint32_t ncmd = __shfl_sync(0xffffffffu, cur.w, 0);
+      const uint32_t hw = __shfl_sync(0xffffffffu, cur.w, 0);
+      const uint32_t ncmd = BC ? (hw & 0xFFu) : hw;
       if (k >= tl.stages) mbar_wait(smem_u32(&empty[s]), (uint32_t)(((k / tl.stages) - 1) & 1));
-      unsigned char* st = tsm + (size_t)s * tl.stage_bytes;
+      unsigned char* st = BC ? tsm : tsm + (size_t)s * tl.stage_bytes;  // BC records: absolute offsets
       const uint32_t bar = smem_u32(&full[s]);
       if (lane == 0) {
         tile_len[s] = (int)L;
+        tile_own[s] = BC ? (int)(hw >> 8) : 0;
         tile_chunk[s] = c_cur;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_expect_tx(bar, total);
@@ -532,13 +539,14 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
     const int sw = q % SWR;
     for (int64_t k = 0; k < my_tiles; ++k) {
       const int s = (int)(k % tl.stages);
-      const unsigned char* st = tsm + (size_t)s * tl.stage_bytes;
-      const double2* sV = reinterpret_cast<const double2*>(st);
+      const unsigned char* st = tsm + (size_t)tl.pool_bytes + (size_t)s * tl.stage_bytes;
+      const double2* sV = reinterpret_cast<const double2*>(BC ? tsm : st);
       const double2* sW = reinterpret_cast<const double2*>(st + tl.off_w);
       const double2* sval = reinterpret_cast<const double2*>(st + tl.off_val);
       const uint16_t* slc = reinterpret_cast<const uint16_t*>(st + tl.off_lcol);
       mbar_wait(smem_u32(&full[s]), (uint32_t)((k / tl.stages) & 1));
       const int L = tile_len[s];
+      const int own_row = tile_own[s];  // 0 unless BC
       const int64_t c = tile_chunk[s];
       for (int gq = g0; gq < G; gq += NCWG) {
         const int kr = gq * RW + q;
@@ -574,7 +582,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
           }
           j = 1;
         }
-        const bool own0 = PEEL && li0 == kr * R;
+        const bool own0 = PEEL && li0 == (own_row + kr) * R;
         for (; j + U <= L; j += U) {  // full batches: no predication
           double2 h[U];
           int li[U];
@@ -607,7 +615,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
               st_stream(a.W + p * R + col, u[cc], pol);
               continue;
             }
-            const double2 vi_c = own0 ? x0[cc] : sV[kr * R + col];
+            const double2 vi_c = own0 ? x0[cc] : sV[(own_row + kr) * R + col];
             double2 uu = u[cc];
             uu.x = fma(-a.b, vi_c.x, uu.x);
             uu.y = fma(-a.b, vi_c.y, uu.y);
@@ -676,7 +684,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
 
 enum Feed { kDirect = 0, kStaged = 1, kTiled = 2 };
 
-template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true, int MINB = 1>
+template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true, int MINB = 1, bool BC = false>
 struct Variant {
   static cudaError_t launch(bool init, const SweepArgs& a, int grid, cudaStream_t s) {
     if constexpr (FEED == kStaged) {
@@ -685,9 +693,9 @@ struct Variant {
       else
         aug_spmmv_staged<R, LPR, U, false><<<grid, kThreads, kStagedSmem, s>>>(a);
     } else if constexpr (FEED == kTiled) {
-      const int smem = a.tl.stages * a.tl.stage_bytes;
-      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB>;
-      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB>;
+      const int smem = a.tl.pool_bytes + a.tl.stages * a.tl.stage_bytes;
+      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB, BC>;
+      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB, BC>;
       cudaFuncSetAttribute(k_init, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       (init ? k_init : k_main)<<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
@@ -704,7 +712,7 @@ struct Variant {
     if constexpr (FEED == kStaged) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_staged<R, LPR, U, false>, kThreads, kStagedSmem);
     } else if constexpr (FEED == kTiled) {
-      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB>;
+      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB, BC>;
       cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_main, tiled_threads<LPR, CS>(), dyn_smem);
     } else {
@@ -724,6 +732,7 @@ struct Entry {
   LaunchFn launch;
   OccFn occ;
   int stages = 0;  // tiled feed: preferred ring depth (0 = plan_tiles default)
+  int bc_ctas = 0;  // block-cache feed: CTAs per SM its shared-memory plan is sized for (0: not BC)
 };
 #define KPM_VARIANT(R, LPR, U, F, NAME) {R, NAME, F, true, Variant<R, LPR, U, F>::launch, Variant<R, LPR, U, F>::occupancy}
 #define KPM_VARIANT_CS(R, LPR, U, CS, NAME) \
@@ -756,6 +765,8 @@ const Entry kTable[] = {
     KPM_VARIANT(8, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kDirect, "direct.lpr8.u4"),
     KPM_VARIANT_WR_S(16, 4, 4, 2, "tiled.lpr4.u4.wr.s2"),
+    {16, "tiled.bc.lpr4.u4.wr", kTiled, false, Variant<16, 4, 4, kTiled, 1, false, 2, true>::launch,
+     Variant<16, 4, 4, kTiled, 1, false, 2, true>::occupancy, 2, 2},
     KPM_VARIANT(16, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(16, 4, 2, kTiled, "tiled.lpr4.u2"),
     KPM_VARIANT_WR(16, 8, 4, "tiled.lpr8.u4.wr"),
@@ -770,6 +781,8 @@ const Entry kTable[] = {
     KPM_VARIANT(32, 8, 2, kTiled, "tiled.lpr8.u2"),
     KPM_VARIANT(32, 16, 4, kStaged, "staged.lpr16.u4"),
     KPM_VARIANT(32, 8, 2, kDirect, "direct.lpr8.u2"),
+    {32, "tiled.bc.lpr8.u4", kTiled, true, Variant<32, 8, 4, kTiled, 1, true, 1, true>::launch,
+     Variant<32, 8, 4, kTiled, 1, true, 1, true>::occupancy, 2, 1},
 };
 
 const Entry* find(int R, int variant) {
@@ -807,6 +820,11 @@ int variant_stages(int R, int variant) {
   return e ? e->stages : 0;
 }
 
+int variant_bc(int R, int variant) {
+  const Entry* e = find(R, variant);
+  return e ? e->bc_ctas : 0;
+}
+
 bool variant_wstage(int R, int variant) {
   const Entry* e = find(R, variant);
   return e && e->wstage;
@@ -830,6 +848,33 @@ TileLayout plan_tiles(int R, int64_t max_other, int64_t max_width, int stages, b
   tl.off_w = (int)v;
   tl.off_val = (int)(v + w);
   tl.off_lcol = (int)(v + w + val);
+  return tl;
+}
+
+// Block-cache layout: a stage = [kBcExtraRows V rows | W | val | lcol], rounded to V rows; the
+// pool takes the rest of the budget in 32-row blocks: at least 5 S, so that S tiles without
+// any reuse (TI: own + 4 neighbour blocks each) can be in flight.
+constexpr int kBcExtraRows = 8;
+TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas) {
+  TileLayout tl;
+  const int64_t rowb = 16ll * R;
+  const int S = stages > 0 ? stages : 2;
+  auto up = [&](int64_t b) { return (b + rowb - 1) / rowb * rowb; };
+  const int64_t extra = kBcExtraRows * rowb;
+  const int64_t w = with_w ? kC * rowb : 0;
+  const int64_t val = round128(kC * max_width * 16), lc = round128(kC * max_width * 2);
+  const int64_t stage = up(extra + w + val + lc);
+  const int64_t pool = kTileBudget / std::max(ctas, 1) - (ctas > 1 ? 4096 : 0) - S * stage;
+  const int P = (int)std::min<int64_t>(kBcMaxSlots, pool / (kC * rowb));
+  if (P < 5 * S) return tl;
+  tl.stages = S;
+  tl.stage_bytes = (int)stage;
+  tl.off_w = (int)extra;
+  tl.off_val = (int)(extra + w);
+  tl.off_lcol = (int)(extra + w + val);
+  tl.pool_slots = P;
+  tl.pool_bytes = (int)(P * kC * rowb);
+  tl.extra_rows = kBcExtraRows;
   return tl;
 }
 

@@ -96,6 +96,14 @@ struct kpm_ctx {
   cudaGraphExec_t graph_exec = nullptr;
   std::vector<int64_t> graph_key;
   int64_t matrix_gen = 0;           // bumped by every kpm_set_matrix / kpm_set_chunk_order
+  // block-cache feed (single rank): per-position records, tile maps, absolute tile rows
+  uint4* bc_rec = nullptr;
+  int* bc_map = nullptr;
+  uint16_t* bc_lcol = nullptr;
+  int* bc_fail = nullptr;
+  size_t bc_rec_cap = 0, bc_map_cap = 0, bc_lcol_cap = 0, bc_fail_cap = 0;
+  std::vector<int64_t> bc_key;      // (R, grid, matrix_gen, stages) the buffers were built for
+  bool bc_ok = false;
   double last_total_ms = 0.0, last_sweep_ms = 0.0;
   int last_n_sweeps = 0;
 };
@@ -223,6 +231,10 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   cudaFree(ctx->halo_rows);
   for (auto& kv : ctx->ipc_open) cudaIpcCloseMemHandle(kv.second);
   cudaFree(ctx->order_list);
+  cudaFree(ctx->bc_rec);
+  cudaFree(ctx->bc_map);
+  cudaFree(ctx->bc_lcol);
+  cudaFree(ctx->bc_fail);
   cudaFree(ctx->flags);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
@@ -824,6 +836,9 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     return plan_tiled_feed(ctx, Rk, with_w, pref_stages, plan);
   };
   auto usable = [&](int v) {
+    if (variant_bc(Rk, v))  // block cache: single rank, fits the layout
+      return ctx->opt.nranks == 1 && s.tiles_ok && s.n_halo == 0 &&
+             plan_tiles_bc(Rk, s.max_width, variant_wstage(Rk, v), variant_stages(Rk, v), variant_bc(Rk, v)).stages >= 1;
     if (variant_tiled(Rk, v)) {
       TileLayout pl;
       return tiled_plan(variant_wstage(Rk, v), variant_stages(Rk, v), pl) == KPM_OK && pl.stages >= 1;
@@ -837,15 +852,46 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     for (variant = 0; variant < variant_count(Rk) - 1 && !usable(variant); ++variant) {
     }
   TileLayout plan;
-  if (variant_tiled(Rk, variant) &&
-      (st = tiled_plan(variant_wstage(Rk, variant), variant_stages(Rk, variant), plan)) != KPM_OK)
+  const bool bc = variant_bc(Rk, variant) > 0;
+  if (bc)
+    plan = plan_tiles_bc(Rk, s.max_width, variant_wstage(Rk, variant), variant_stages(Rk, variant),
+                         variant_bc(Rk, variant));
+  else if (variant_tiled(Rk, variant) &&
+           (st = tiled_plan(variant_wstage(Rk, variant), variant_stages(Rk, variant), plan)) != KPM_OK)
     return st;
   const int rec_index = 2 * lg + (variant_wstage(Rk, variant) ? 1 : 0);
   ctx->last_variant = variant_name(Rk, variant);
   const TileLayout tl = plan;
-  const int dyn_smem = variant_tiled(Rk, variant) ? tl.stages * tl.stage_bytes : 0;
+  const int dyn_smem = variant_tiled(Rk, variant) ? tl.pool_bytes + tl.stages * tl.stage_bytes : 0;
   const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, sweep_occupancy(Rk, variant, dyn_smem));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * occ, s.n_chunks));
+  if (bc) {  // per-position records for this grid and chunk order (built once, cached)
+    const std::vector<int64_t> key = {Rk, grid, ctx->matrix_gen, tl.stages, variant_wstage(Rk, variant) ? 1 : 0};
+    if (key != ctx->bc_key) {
+      ctx->bc_key.clear();
+      if (reserve((void**)&ctx->bc_rec, &ctx->bc_rec_cap, sizeof(uint4) * kRecSlots * s.n_chunks) != cudaSuccess ||
+          reserve((void**)&ctx->bc_map, &ctx->bc_map_cap, sizeof(int) * kBcMapInts * s.n_chunks) != cudaSuccess ||
+          reserve((void**)&ctx->bc_lcol, &ctx->bc_lcol_cap, sizeof(uint16_t) * s.n_slots) != cudaSuccess ||
+          reserve((void**)&ctx->bc_fail, &ctx->bc_fail_cap, sizeof(int)) != cudaSuccess)
+        return fail(ctx, KPM_ENOMEM, "block-cache plan buffers");
+      KPM_CUDA(cudaMemsetAsync(ctx->bc_fail, 0, sizeof(int), ctx->stream));
+      KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->order_list, s.n_chunks, grid, Rk,
+                               variant_wstage(Rk, variant), tl, ctx->bc_rec, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail,
+                               ctx->stream));
+      int hfail = 0;
+      KPM_CUDA(cudaMemcpyAsync(&hfail, ctx->bc_fail, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      KPM_CUDA(cudaStreamSynchronize(ctx->stream));
+      ctx->bc_ok = hfail == 0;
+      ctx->bc_key = key;
+    }
+    if (!ctx->bc_ok) {  // some tile does not fit the pool: rerun with the width's default variant
+      const int saved = ctx->variant_override;
+      ctx->variant_override = 0;
+      const kpm_status r = run_block(ctx, M, rb, col_begin, seed, v0, eta_cols, first, last);
+      ctx->variant_override = saved;
+      return r;
+    }
+  }
   const bool multi = ctx->opt.nranks > 1;
   const int parts = multi ? 2 : 1;  // edge + interior launches per sweep
   const size_t per_sweep = (size_t)3 * Rk * grid * parts;
@@ -889,8 +935,8 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   sa.chunk_list = ctx->order_list;  // NULL: storage order
   sa.chunk_begin = 0;
   sa.chunk_end = s.n_chunks;
-  sa.rec = s.rec[rec_index];
-  sa.lcol = s.lcol;
+  sa.rec = bc ? ctx->bc_rec : s.rec[rec_index];
+  sa.lcol = bc ? ctx->bc_lcol : s.lcol;
   sa.tl = tl;
   sa.b = ctx->b;
   sa.pstride = (int64_t)grid * parts;
@@ -1265,6 +1311,8 @@ extern "C" kpm_status kpm_last_timing(const kpm_ctx* ctx, double* total_ms, doub
 }
 
 extern "C" const char* kpm_last_kernel(const kpm_ctx* ctx) { return ctx ? ctx->last_variant.c_str() : ""; }
+
+extern "C" const char* kpm_variant_name(int R, int variant) { return kpm::variant_name(R, variant); }
 
 extern "C" kpm_status kpm_get_sell_info(const kpm_ctx* ctx, kpm_sell_info* info) {
   if (!ctx || !info) return KPM_EINVAL;

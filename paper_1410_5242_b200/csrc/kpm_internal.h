@@ -56,7 +56,13 @@ struct TileLayout {
   int stages = 0;
   int stage_bytes = 0;
   int off_w = 0, off_val = 0, off_lcol = 0;  // V tile rows start at 0
+  // block-cache feed only: dynamic shared memory = [pool of pool_slots blocks of
+  // 32 V rows][stage 0]..[stage S-1]; a stage holds [extra_rows V rows | W | val | lcol] and
+  // starts at pool_bytes + s * stage_bytes; all offsets are multiples of one V row (16 R bytes)
+  int pool_bytes = 0, pool_slots = 0, extra_rows = 0;
 };
+constexpr int kBcMaxSlots = 16;  // block-cache pool slots (max)
+constexpr int kBcMapInts = 40;   // per tile: [n_blocks, (block, smem row) x 7, -, n_extra, (row, count, smem row) x 8]
 
 // Fused halo exchange: rows [pos, pos+count) of the new W are also stored to dst (a peer
 // GPU's halo slots, mapped over NVLink with CUDA IPC) by the sweep kernel's epilogue.
@@ -151,6 +157,15 @@ int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val,
                       int64_t row_end, int64_t n_global, DevSell& d, DeviceBuild& out, BuildScratch& ws,
                       std::string& err, cudaStream_t s);
 // Copy records of the tiled feed for block width R from the per-chunk run lists.
+// Block-cache feed: per-position copy records (kRecSlots uint4, list position b + G k = CTA b's
+// k-th tile) from a simulation of each CTA's pool of 32-row V blocks, and the tile-row index
+// of every SELL slot pointing into that CTA's shared memory.  *fail != 0 if some tile does not fit.
+cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* runs, const int* scol,
+                            const int64_t* list, int64_t n_chunks, int grid, int R, bool with_w,
+                            const TileLayout& tl, uint4* rec, int* map, uint16_t* lcol_bc, int* fail,
+                            cudaStream_t s);
+TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas);
+int variant_bc(int R, int variant);  // block-cache feed: CTAs per SM it is planned for, 0 = other feed
 cudaError_t launch_build_records(const int64_t* cptr, const int* nruns, const int* runs, int64_t n_chunks, int R,
                                  int off_w, int off_val, int off_lcol, uint4* rec, cudaStream_t s);
 

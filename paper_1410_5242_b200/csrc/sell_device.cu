@@ -276,12 +276,158 @@ __global__ void build_records_kernel(const int64_t* __restrict__ cptr, const int
   }
 }
 
+// Block-cache records: one thread per CTA simulates that CTA's pool of 32-row V blocks over its
+// tile sequence (list positions b, b + G, b + 2G, ...).  A tile needs its own block and every
+// block-aligned full 32-row run of its other rows (pool), the remaining rows are copied per
+// stage (extra rows).  A slot may be refilled for tile k only if its last user is tile k - S or
+// older: the producer refills stage k % S after all warps released tile k - S (ring order).
+__global__ void bc_plan_kernel(const int64_t* __restrict__ cptr, const int* __restrict__ nruns,
+                               const int* __restrict__ runs, const int64_t* __restrict__ list, int64_t n_chunks, int G,
+                               int R, int with_w, TileLayout tl, uint4* __restrict__ rec, int* __restrict__ map,
+                               int* __restrict__ fail) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= G) return;
+  int sblk[kBcMaxSlots];
+  int64_t slast[kBcMaxSlots];
+  for (int i = 0; i < kBcMaxSlots; ++i) {
+    sblk[i] = -1;
+    slast[i] = -(1ll << 40);
+  }
+  const int64_t rowb = 16ll * R, blkb = 32 * rowb;
+  const int S = tl.stages, P = tl.pool_slots;
+  for (int64_t k = 0; b + k * G < n_chunks; ++k) {
+    const int64_t pos = b + k * G;
+    const int64_t c = list ? list[pos] : pos;
+    const int64_t stage = tl.pool_bytes + (k % S) * (int64_t)tl.stage_bytes;
+    uint4* r = rec + pos * kRecSlots;
+    int* m = map + pos * kBcMapInts;
+    bool ok = true;
+    int n = 0;
+    int64_t total = 0, wbytes = 0;
+    auto cmd = [&](uint32_t base, int64_t src, int64_t dst, int64_t bytes) {
+      if (n + 1 >= kRecSlots) {
+        ok = false;
+        return;
+      }
+      ++n;
+      r[n] = make_uint4((uint32_t)src, (uint32_t)((uint64_t)src >> 32), (uint32_t)dst, (uint32_t)bytes | (base << 28));
+      total += bytes;
+    };
+    int need[7], nneed = 0, xs[8], xc[8], nx = 0;
+    need[nneed++] = (int)c;  // own rows = block c
+    for (int q = 0; q < nruns[c]; ++q) {
+      int first = runs[c * 2 * kMaxRuns + 2 * q], cnt = runs[c * 2 * kMaxRuns + 2 * q + 1];
+      while (cnt > 0) {
+        if ((first & 31) == 0 && cnt >= 32) {
+          if (nneed < 7) need[nneed++] = first >> 5; else ok = false;
+          first += 32;
+          cnt -= 32;
+        } else {
+          const int piece = min(cnt, 32 - (first & 31));
+          if (nx < 8) {
+            xs[nx] = first;
+            xc[nx] = piece;
+            ++nx;
+          } else {
+            ok = false;
+          }
+          first += piece;
+          cnt -= piece;
+        }
+      }
+    }
+    m[0] = nneed;
+    for (int i = 0; i < nneed && ok; ++i) {
+      int slot = -1;
+      for (int p = 0; p < P; ++p)
+        if (sblk[p] == need[i]) slot = p;
+      if (slot < 0) {
+        int64_t best = 1ll << 62;
+        for (int p = 0; p < P; ++p)
+          if (slast[p] <= k - S && slast[p] < best) {
+            best = slast[p];
+            slot = p;
+          }
+        if (slot < 0) {
+          ok = false;
+          break;
+        }
+        sblk[slot] = need[i];
+        cmd(0, (int64_t)need[i] * blkb, (int64_t)slot * blkb, blkb);
+      }
+      slast[slot] = k;
+      m[1 + 2 * i] = need[i];
+      m[2 + 2 * i] = slot * 32;
+    }
+    m[15] = nx;
+    int64_t erow = 0;
+    for (int i = 0; i < nx && ok; ++i) {
+      if (erow + xc[i] > tl.extra_rows) {
+        ok = false;
+        break;
+      }
+      const int64_t dst = stage + erow * rowb;
+      cmd(0, (int64_t)xs[i] * rowb, dst, xc[i] * rowb);
+      m[16 + 3 * i] = xs[i];
+      m[17 + 3 * i] = xc[i];
+      m[18 + 3 * i] = (int)(dst / rowb);
+      erow += xc[i];
+    }
+    const int64_t s0 = cptr[c], nslot = cptr[c + 1] - s0;
+    if (with_w) {
+      cmd(1, c * blkb, stage + tl.off_w, blkb);
+      wbytes = blkb;
+    }
+    if (nslot) {
+      cmd(2, s0 * 16, stage + tl.off_val, nslot * 16);
+      cmd(3, s0 * 2, stage + tl.off_lcol, nslot * 2);
+    }
+    for (int q = n + 1; q < kRecSlots; ++q) r[q] = make_uint4(0u, 0u, 0u, 0u);
+    r[0] = make_uint4((uint32_t)total, (uint32_t)(total - wbytes), (uint32_t)(nslot / kC),
+                      (uint32_t)n | ((uint32_t)m[2] << 8));
+    if (!ok) atomicOr(fail, 1);
+  }
+}
+
+// Tile-row index (absolute shared-memory V row) of every SELL slot, one warp per tile.
+__global__ void bc_lcol_kernel(const int* __restrict__ scol, const int64_t* __restrict__ cptr,
+                               const int64_t* __restrict__ list, int64_t n_chunks, const int* __restrict__ map,
+                               uint16_t* __restrict__ lcol, int* __restrict__ fail) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t pos = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); pos < n_chunks; pos += warps) {
+    const int64_t c = list ? list[pos] : pos;
+    const int* m = map + pos * kBcMapInts;
+    const int nb = min(m[0], 7), nx = min(m[15], 8);
+    for (int64_t e = cptr[c] + lane; e < cptr[c + 1]; e += 32) {
+      const int g = scol[e];
+      int row = -1;
+      for (int i = 0; i < nb; ++i)
+        if (m[1 + 2 * i] == (g >> 5)) row = m[2 + 2 * i] + (g & 31);
+      for (int i = 0; i < nx && row < 0; ++i)
+        if (g >= m[16 + 3 * i] && g < m[16 + 3 * i] + m[17 + 3 * i]) row = m[18 + 3 * i] + g - m[16 + 3 * i];
+      if (row < 0 || row > 65535) atomicOr(fail, 2);
+      lcol[e] = (uint16_t)max(row, 0);
+    }
+  }
+}
+
 int grid_for(int64_t n, int block) {
   const int64_t g = (n + block - 1) / block;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
 }
 
 }  // namespace
+
+cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* runs, const int* scol,
+                            const int64_t* list, int64_t n_chunks, int grid, int R, bool with_w,
+                            const TileLayout& tl, uint4* rec, int* map, uint16_t* lcol_bc, int* fail,
+                            cudaStream_t s) {
+  bc_plan_kernel<<<(grid + 63) / 64, 64, 0, s>>>(cptr, nruns, runs, list, n_chunks, grid, R, with_w ? 1 : 0, tl, rec,
+                                                  map, fail);
+  bc_lcol_kernel<<<grid_for(n_chunks * 32, 256), 256, 0, s>>>(scol, cptr, list, n_chunks, map, lcol_bc, fail);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_build_records(const int64_t* cptr, const int* nruns, const int* runs, int64_t n_chunks, int R,
                                  int off_w, int off_val, int off_lcol, uint4* rec, cudaStream_t s) {

@@ -2,7 +2,7 @@
 CTA b processes the 5 z-blocks of one (x, y) column in consecutive tiles (so a tile's z-runs
 come from its own previous / next tile), with board power and SM clock sampled.
 
-    python scripts/exp_order.py <storage|zcol> <R> <grid>      # on the GPU box
+    python scripts/exp_order.py <storage|zcol|ylines> <R> <grid>      # on the GPU box (KPM_VARIANT honoured)
 """
 import json
 import os
@@ -38,6 +38,11 @@ def main():
         n_chunks = lat.n // 32
         if mode == "zcol":
             ctx.set_chunk_order(zcol_order(n_chunks, 5, G))
+        elif mode == "ylines":
+            from workloads.ti_lattice import chunk_order_ylines
+            ctx.set_chunk_order(chunk_order_ylines(lat, G))
+        ctx.moments(8, R, SEED, want_eta=False)
+        short = ctx.last_timing()[1]
         t0 = time.time()
         while time.time() - t0 < 5.0:
             mu0, _ = ctx.moments(2000, R, SEED, want_eta=False)
@@ -47,6 +52,7 @@ def main():
         for _ in range(4):
             mu, _ = ctx.moments(2000, R, SEED, want_eta=False)
             sweeps.append(ctx.last_timing()[1])
+        kern = ctx.last_kernel()
         smi.terminate()
         out = smi.communicate()[0]
     pw, mhz = [], []
@@ -59,7 +65,7 @@ def main():
             pass
     pw.sort()
     mhz.sort()
-    print(json.dumps(dict(order=mode, R=R, grid=G, sweep_ms=sorted(sweeps)[2], power_w=pw[len(pw) // 2],
+    print(json.dumps(dict(order=mode, R=R, grid=G, kernel=kern, short_sweep_ms=short, sweep_ms=sorted(sweeps)[2], power_w=pw[len(pw) // 2],
                           sm_mhz=mhz[len(mhz) // 2], mu2=float(mu[2]))), flush=True)
 
 

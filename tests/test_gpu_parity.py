@@ -213,14 +213,17 @@ def test_every_kernel_variant(pkg, R, monkeypatch):
     M = 48
     eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, SEED)
     seen = set()
-    for v in range(12):
+    for v in range(16):
+        want = pkg.variant_name(R, v)
+        if want is None:
+            break
         monkeypatch.setenv("KPM_VARIANT", str(v))
         with pkg.KpmContext() as ctx:
             ctx.set_matrix(rp, col, val, a, b)
             mu, eta = ctx.moments(M, R, SEED)
             name = ctx.last_kernel()
-        if name in seen:
-            break  # index past the last variant falls back to the default
+        # only a variant whose plan cannot fit this matrix (block cache, staged) falls back
+        assert name == want or ".bc." in want or want.startswith("staged"), (want, name)
         seen.add(name)
         check(eta, mu, eta_o)
     assert len(seen) >= 2
@@ -332,6 +335,31 @@ def test_rows_without_diagonal(pkg, R):
             s = ctx.export_sell()
         check(eta, mu, eta_o)
         assert np.array_equal(s["col"], ref["col"]) and np.array_equal(s["val"], ref["val"])
+
+
+@pytest.mark.parametrize("ordered", [False, True])
+@pytest.mark.parametrize("R,dims,name,ctas", [(32, (40, 20, 32), "tiled.bc.lpr8.u4", 1),
+                                             (16, (80, 12, 32), "tiled.bc.lpr4.u4.wr", 2)])
+def test_block_cache_feed(pkg, monkeypatch, ordered, R, dims, name, ctas):
+    """Block-cache feed (tiled.bc): per-CTA pools of 32-row V blocks reused across tiles.  On
+    lattices with more z-block lines than CTAs (one lock-stepped round + a storage-order tail),
+    with and without the y-line order: oracle-exact, and the variant really ran."""
+    import torch
+
+    from workloads.ti_lattice import chunk_order_ylines
+
+    lat, rp, col, val, a, b = problem(dims)
+    M = 24
+    idx = [pkg.variant_name(R, v) for v in range(16)].index(name)
+    monkeypatch.setenv("KPM_VARIANT", str(idx))
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        if ordered:
+            sms = torch.cuda.get_device_properties(0).multi_processor_count
+            ctx.set_chunk_order(chunk_order_ylines(lat, ctas * sms))
+        mu, eta = ctx.moments(M, R, SEED)
+        assert ctx.last_kernel() == name
+    check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, M, R, SEED))
 
 
 @pytest.mark.parametrize("R", [1, 8, 32])

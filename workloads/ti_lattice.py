@@ -308,6 +308,32 @@ def chunk_order_yband(lat: Lattice, x0: int, x1: int, band: int, C: int = 32):
     return np.concatenate(order).astype(np.int64)
 
 
+def chunk_order_ylines(lat: Lattice, grid: int, C: int = 32):
+    """Locality hint for kpm_set_chunk_order and the block-cache feed (not method arithmetic):
+    list position b + grid*k is CTA b's k-th tile.  In full rounds of `grid` lines, CTA b
+    walks one y-line of chunks (x, 0..Ny-1, z-block), all CTAs in step at the same y, so
+    consecutive tiles of a CTA share their y-neighbour blocks and the x-neighbour blocks are
+    other CTAs' current own blocks (L2 hits).  The lines left over after the last full round
+    follow in storage order (no reuse, perfect balance)."""
+    if (4 * lat.nz) % C:
+        raise ValueError("needs 8 | Nz so chunks align with z-columns")
+    zb = 4 * lat.nz // C
+    n_lines = lat.nx * zb
+    rounds = n_lines // grid
+    parts = []
+    y = np.arange(lat.ny)
+    for r in range(rounds):
+        line = r * grid + np.arange(grid)
+        x, z = line // zb, line % zb
+        parts.append(((x[None, :] * lat.ny + y[:, None]) * zb + z[None, :]).ravel())
+    done = rounds * grid
+    if done < n_lines:
+        line = np.arange(done, n_lines)
+        x, z = line // zb, line % zb
+        parts.append(np.sort(((x[:, None] * lat.ny + y[None, :]) * zb + z[:, None]).ravel()))
+    return np.concatenate(parts).astype(np.int64)
+
+
 # ---- configurations of BASELINE.json (SURVEY §8(d)) ----------------------------------
 CONFIGS = {
     "C1": dict(lattice=(8, 8, 8), M=64, R=4),
