@@ -31,7 +31,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from workloads.ti_lattice import (CONFIGS, SEED, Lattice, chunk_order_yband, gershgorin, generate_csr,  # noqa: E402
+from workloads.ti_lattice import (CONFIGS, SEED, Lattice, chunk_order_yband, chunk_order_ylines, gershgorin, generate_csr,  # noqa: E402
                                   generate_csr_torch, scale_factors)
 
 S_D, S_I = 16, 4
@@ -227,7 +227,7 @@ def main():
                          "global size fixed (strong scaling over N); C5: 1800x400x40 slab per GPU (~150 GB HBM), "
                          "M=4000, generated and converted on the GPU (weak scaling)")
     ap.add_argument("--chunk-order", default="auto", choices=["auto", "none"],
-                    help="auto: y-banded chunk order when the x-neighbour window exceeds ~32 MB (kpm_set_chunk_order)")
+                    help="auto: y-banded chunk order when the x-neighbour window exceeds ~32 MB, else (1 GPU) y-line walks for the block-cache feed (kpm_set_chunk_order)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-r-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -309,14 +309,27 @@ def main():
         del rp, col, val
         torch.cuda.empty_cache()
     band = None
+    order = None
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+
+    def yline_order(r):  # the block-cache feed runs 1 CTA per SM at R = 32 and 2 at R = 16 (kernels.cu)
+        return chunk_order_ylines(lat, sms * (2 if r == 16 else 1))
+
+    use_lines = False
     if args.chunk_order == "auto" and 2 * lat.rows_per_plane * min(R, 32) * 16 > 32e6 and lat.nz % 8 == 0:
         band = max(1, int(16e6 // (2 * 4 * nz * min(R, 32) * 16)))
         order = chunk_order_yband(lat, x0, x1, band)
+    elif args.chunk_order == "auto" and world == 1 and lat.nz % 8 == 0 and lat.nx * (lat.nz // 8) >= 2 * sms:
+        # y-line walks in lock-stepped rounds: consecutive tiles of a CTA share y-neighbour blocks,
+        # which the block-cache feed keeps in shared memory
+        use_lines = True
+        order = yline_order(R)
 
-        def apply_order():
+    def apply_order():
+        if order is not None:
             ctx.set_chunk_order(order)
 
-        apply_order()
+    apply_order()
     n_blocks = (R + 31) // 32
 
     for _ in range(args.warmup):
@@ -353,7 +366,7 @@ def main():
         "scaling": scaling, "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": w["name"],
                    "lattice": [nx, ny, nz], "N": n, "N_nz": nnz, "M": M, "R": R, "parallelism": f"x-slab dp{world}",
-                   "hbm_in_use_gb": round((total_b - free_b) / 1e9, 1), "kernel_variant": ctx.last_kernel(), "chunk_order": f"y-band {band}" if band else "storage", "halo": os.environ.get("KPM_HALO", "fused") if world > 1 else None,
+                   "hbm_in_use_gb": round((total_b - free_b) / 1e9, 1), "kernel_variant": ctx.last_kernel(), "chunk_order": f"y-band {band}" if band else ("y-lines" if use_lines else "storage"), "halo": os.environ.get("KPM_HALO", "fused") if world > 1 else None,
                    "l2": ("inputs larger than L2 (V, W %.2f GB each per GPU; matrix %.2f GB)" if
                           (32 * R * n_loc + 20 * nnz_loc) > 126e6 else
                           "L2-resident working set (V, W %.2f GB each, matrix %.2f GB; no flush)") % (
@@ -371,6 +384,8 @@ def main():
     if not args.no_r_sweep and world == 1:
         by_r = {}
         for r in (1, 2, 4, 8, 16, 32):
+            if use_lines:  # only the block-cache widths walk y-lines; the others keep storage order
+                ctx.set_chunk_order(yline_order(r) if r >= 16 else None)
             ctx.moments(200, r, SEED, want_eta=False)
             ctx.moments(200, r, SEED, want_eta=False)
             sw = ctx.last_timing()[1]
@@ -415,15 +430,13 @@ def main():
         h2d = rp.nbytes + col.nbytes + val.nbytes
         d2h = M * 8 + R * M * 16
         ctx.set_matrix(prp, pcol, pval, a, b, n_global=n, row_begin=row_begin)  # warm-up: first DMA from these pages
-        if band:
-            apply_order()
+        apply_order()
         barrier()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 1)]
         ev[0].record(stream)
         for i in range(args.steps):
             ctx.set_matrix(prp, pcol, pval, a, b, n_global=n, row_begin=row_begin)
-            if band:
-                apply_order()
+            apply_order()
             ev[2 * i + 1].record(stream)
             ctx.moments(M, R, SEED, want_eta=True)
             ev[2 * i + 2].record(stream)

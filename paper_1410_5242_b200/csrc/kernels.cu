@@ -744,7 +744,9 @@ struct Entry {
    Variant<R, LPR, U, kTiled, 1, false, (R <= 8 ? 3 : 2)>::occupancy, S}
 #define KPM_VARIANT_WR(R, LPR, U, NAME) \
   {R, NAME, kTiled, false, Variant<R, LPR, U, kTiled, 1, false>::launch, Variant<R, LPR, U, kTiled, 1, false>::occupancy}
-// First entry of each width is the default (chosen from the B200 measurements in DESIGN.md).
+// First entry of each width is the default (chosen from the B200 measurements in DESIGN.md); at
+// R = 16 and 32 that is the block-cache feed, single rank only, and the first other entry
+// (base_variant) is what runs where it cannot (several ranks, a plan that does not fit).
 const Entry kTable[] = {
     KPM_VARIANT(1, 1, 4, kTiled, "tiled.lpr1.u4"),
     KPM_VARIANT(1, 1, 4, kDirect, "direct.lpr1.u4"),
@@ -764,9 +766,9 @@ const Entry kTable[] = {
     KPM_VARIANT(8, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kDirect, "direct.lpr8.u4"),
-    KPM_VARIANT_WR_S(16, 4, 4, 2, "tiled.lpr4.u4.wr.s2"),
     {16, "tiled.bc.lpr4.u4.wr", kTiled, false, Variant<16, 4, 4, kTiled, 1, false, 2, true>::launch,
      Variant<16, 4, 4, kTiled, 1, false, 2, true>::occupancy, 2, 2},
+    KPM_VARIANT_WR_S(16, 4, 4, 2, "tiled.lpr4.u4.wr.s2"),
     KPM_VARIANT(16, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(16, 4, 2, kTiled, "tiled.lpr4.u2"),
     KPM_VARIANT_WR(16, 8, 4, "tiled.lpr8.u4.wr"),
@@ -775,14 +777,14 @@ const Entry kTable[] = {
     KPM_VARIANT_CS(16, 8, 4, 2, "tiled.lpr8.u4.cs2"),
     KPM_VARIANT(16, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(16, 8, 4, kDirect, "direct.lpr8.u4"),
+    {32, "tiled.bc.lpr8.u4", kTiled, true, Variant<32, 8, 4, kTiled, 1, true, 1, true>::launch,
+     Variant<32, 8, 4, kTiled, 1, true, 1, true>::occupancy, 2, 1},
     KPM_VARIANT(32, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT_WR(32, 8, 4, "tiled.lpr8.u4.wr"),
     KPM_VARIANT_CS(32, 8, 4, 2, "tiled.lpr8.u4.cs2"),
     KPM_VARIANT(32, 8, 2, kTiled, "tiled.lpr8.u2"),
     KPM_VARIANT(32, 16, 4, kStaged, "staged.lpr16.u4"),
     KPM_VARIANT(32, 8, 2, kDirect, "direct.lpr8.u2"),
-    {32, "tiled.bc.lpr8.u4", kTiled, true, Variant<32, 8, 4, kTiled, 1, true, 1, true>::launch,
-     Variant<32, 8, 4, kTiled, 1, true, 1, true>::occupancy, 2, 1},
 };
 
 const Entry* find(int R, int variant) {
@@ -818,6 +820,16 @@ bool variant_tiled(int R, int variant) {
 int variant_stages(int R, int variant) {
   const Entry* e = find(R, variant);
   return e ? e->stages : 0;
+}
+
+int base_variant(int R) {
+  int i = 0;
+  for (const Entry& e : kTable)
+    if (e.R == R) {
+      if (!e.bc_ctas) return i;
+      ++i;
+    }
+  return 0;
 }
 
 int variant_bc(int R, int variant) {
@@ -906,7 +918,7 @@ struct KindEntry {
   int R;
   KindFn nodot, spmmv;
 };
-// keep in step with the defaults at the head of each width in kTable
+// keep in step with base_variant(R) of each width in kTable
 const KindEntry kKinds[] = {
     {1, launch_kind<1, 1, true, kAugNoDot>, launch_kind<1, 1, true, kSpmmv>},
     {2, launch_kind<2, 2, true, kAugNoDot>, launch_kind<2, 2, true, kSpmmv>},
@@ -918,8 +930,9 @@ const KindEntry kKinds[] = {
 }  // namespace
 
 cudaError_t launch_sweep_kind(int R, int kind, const SweepArgs& a, int grid, cudaStream_t s) {
-  if (kind == kAug) return launch_aug_spmmv(R, 0, false, a, grid, s);
-  if (!variant_tiled(R, 0)) return cudaErrorInvalidValue;
+  const int bv = base_variant(R);
+  if (kind == kAug) return launch_aug_spmmv(R, bv, false, a, grid, s);
+  if (!variant_tiled(R, bv)) return cudaErrorInvalidValue;
   for (const KindEntry& e : kKinds)
     if (e.R == R) return kind == kAugNoDot ? e.nodot(a, grid, s) : kind == kSpmmv ? e.spmmv(a, grid, s) : cudaErrorInvalidValue;
   return cudaErrorInvalidValue;

@@ -884,9 +884,9 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
       ctx->bc_ok = hfail == 0;
       ctx->bc_key = key;
     }
-    if (!ctx->bc_ok) {  // some tile does not fit the pool: rerun with the width's default variant
+    if (!ctx->bc_ok) {  // some tile does not fit the pool: rerun with the width's base variant
       const int saved = ctx->variant_override;
-      ctx->variant_override = 0;
+      ctx->variant_override = base_variant(Rk);
       const kpm_status r = run_block(ctx, M, rb, col_begin, seed, v0, eta_cols, first, last);
       ctx->variant_override = saved;
       return r;
@@ -1243,12 +1243,13 @@ extern "C" kpm_status kpm_sweep_kernel(kpm_ctx* ctx, int kind, int R, uint64_t s
   if ((st = ensure(ctx, (void**)&ctx->X1, &xcap, (size_t)n_rows_total * R, sizeof(double2))) != KPM_OK) return st;
   ctx->x_cap = xcap;
   TileLayout tl;
-  if (variant_tiled(R, 0) && (st = plan_tiled_feed(ctx, R, variant_wstage(R, 0), variant_stages(R, 0), tl)) != KPM_OK)
+  const int bv = base_variant(R);  // the analysis kernels use the regular tiled feed
+  if (variant_tiled(R, bv) && (st = plan_tiled_feed(ctx, R, variant_wstage(R, bv), variant_stages(R, bv), tl)) != KPM_OK)
     return st;
-  if (!variant_tiled(R, 0) || tl.stages < 1)
+  if (!variant_tiled(R, bv) || tl.stages < 1)
     return fail(ctx, KPM_ESTATE, "the matrix does not fit the tiled feed of the analysis kernels");
   const int dyn_smem = tl.stages * tl.stage_bytes;
-  const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, sweep_occupancy(R, 0, dyn_smem));
+  const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, sweep_occupancy(R, bv, dyn_smem));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * occ, s.n_chunks));
   if ((st = ensure(ctx, (void**)&ctx->partials, &ctx->partials_cap, (size_t)3 * R * grid, sizeof(double))) != KPM_OK)
     return st;
@@ -1263,7 +1264,7 @@ extern "C" kpm_status kpm_sweep_kernel(kpm_ctx* ctx, int kind, int R, uint64_t s
   sa.chunk_list = ctx->order_list;
   sa.chunk_begin = 0;
   sa.chunk_end = s.n_chunks;
-  sa.rec = s.rec[2 * __builtin_ctz(R) + (variant_wstage(R, 0) ? 1 : 0)];
+  sa.rec = s.rec[2 * __builtin_ctz(R) + (variant_wstage(R, bv) ? 1 : 0)];
   sa.lcol = s.lcol;
   sa.tl = tl;
   sa.b = ctx->b;
@@ -1282,7 +1283,7 @@ extern "C" kpm_status kpm_sweep_kernel(kpm_ctx* ctx, int kind, int R, uint64_t s
   KPM_CUDA(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]));
   if (ms_per_sweep) *ms_per_sweep = ms / n_sweeps;
   static const char* kSuffix[] = {"", ".nodot", ".spmmv"};
-  ctx->last_variant = std::string(variant_name(R, 0)) + kSuffix[kind];
+  ctx->last_variant = std::string(variant_name(R, bv)) + kSuffix[kind];
   if (w_out) {  // stored position p holds local row perm[p] (identity when sigma = 1)
     std::vector<double2> wh((size_t)s.n_pad * R);
     KPM_CUDA(cudaMemcpy(wh.data(), ctx->X1, sizeof(double2) * wh.size(), cudaMemcpyDeviceToHost));

@@ -166,6 +166,7 @@ cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* ru
                             cudaStream_t s);
 TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas);
 int variant_bc(int R, int variant);  // block-cache feed: CTAs per SM it is planned for, 0 = other feed
+int base_variant(int R);             // first variant of width R that is not a block-cache feed
 cudaError_t launch_build_records(const int64_t* cptr, const int* nruns, const int* runs, int64_t n_chunks, int R,
                                  int off_w, int off_val, int off_lcol, uint4* rec, cudaStream_t s);
 
