@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--M", type=int, default=8)
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--sigma", type=int, default=1)
+    ap.add_argument("--order", default="ylines", choices=["ylines", "storage"],
+                    help="ylines: the bench's chunk order at R = 16 / 32 (block-cache feed)")
     args = ap.parse_args()
     import paper_1410_5242_b200 as kpm
 
@@ -28,6 +30,12 @@ def main():
     with kpm.KpmContext(sell_sigma=args.sigma) as ctx:
         ctx.set_matrix(rp, col, val, a, b)
         for R in (int(r) for r in args.R.split(",")):
+            if args.order == "ylines":
+                import torch
+
+                from workloads.ti_lattice import chunk_order_ylines
+                sms = torch.cuda.get_device_properties(0).multi_processor_count
+                ctx.set_chunk_order(chunk_order_ylines(lat, sms * (2 if R == 16 else 1)) if R >= 16 else None)
             for _ in range(args.reps):
                 mu, _ = ctx.moments(args.M, R, SEED, want_eta=False)
             t, s, n = ctx.last_timing()
