@@ -313,13 +313,13 @@ def main():
     sms = torch.cuda.get_device_properties(local).multi_processor_count
 
     def yline_order(r):  # the block-cache feed runs 1 CTA per SM at R = 32 and 2 at R = 16 (kernels.cu)
-        return chunk_order_ylines(lat, sms * (2 if r == 16 else 1))
+        return chunk_order_ylines(lat, sms * (2 if r == 16 else 1), x0=x0, x1=x1, edges_last=world > 1)
 
     use_lines = False
     if args.chunk_order == "auto" and 2 * lat.rows_per_plane * min(R, 32) * 16 > 32e6 and lat.nz % 8 == 0:
         band = max(1, int(16e6 // (2 * 4 * nz * min(R, 32) * 16)))
         order = chunk_order_yband(lat, x0, x1, band)
-    elif args.chunk_order == "auto" and world == 1 and lat.nz % 8 == 0 and lat.nx * (lat.nz // 8) >= 2 * sms:
+    elif args.chunk_order == "auto" and R >= 16 and lat.nz % 8 == 0 and (x1 - x0) * (lat.nz // 8) >= 2 * sms:
         # y-line walks in lock-stepped rounds: consecutive tiles of a CTA share y-neighbour blocks,
         # which the block-cache feed keeps in shared memory
         use_lines = True

@@ -97,7 +97,9 @@ struct kpm_ctx {
   std::vector<int64_t> graph_key;
   int64_t matrix_gen = 0;           // bumped by every kpm_set_matrix / kpm_set_chunk_order
   // block-cache feed (single rank): per-position records, tile maps, absolute tile rows
-  uint4* bc_rec = nullptr;
+  uint4* bc_rec = nullptr;           // single rank, or the edge list of several ranks
+  uint4* bc_rec2 = nullptr;          // the interior list of several ranks
+  size_t bc_rec2_cap = 0;
   int* bc_map = nullptr;
   uint16_t* bc_lcol = nullptr;
   int* bc_fail = nullptr;
@@ -232,6 +234,7 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   for (auto& kv : ctx->ipc_open) cudaIpcCloseMemHandle(kv.second);
   cudaFree(ctx->order_list);
   cudaFree(ctx->bc_rec);
+  cudaFree(ctx->bc_rec2);
   cudaFree(ctx->bc_map);
   cudaFree(ctx->bc_lcol);
   cudaFree(ctx->bc_fail);
@@ -836,8 +839,8 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     return plan_tiled_feed(ctx, Rk, with_w, pref_stages, plan);
   };
   auto usable = [&](int v) {
-    if (variant_bc(Rk, v))  // block cache: single rank, fits the layout
-      return ctx->opt.nranks == 1 && s.tiles_ok && s.n_halo == 0 &&
+    if (variant_bc(Rk, v))  // block cache: fits the layout
+      return s.tiles_ok &&
              plan_tiles_bc(Rk, s.max_width, variant_wstage(Rk, v), variant_stages(Rk, v), variant_bc(Rk, v)).stages >= 1;
     if (variant_tiled(Rk, v)) {
       TileLayout pl;
@@ -869,15 +872,35 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     const std::vector<int64_t> key = {Rk, grid, ctx->matrix_gen, tl.stages, variant_wstage(Rk, variant) ? 1 : 0};
     if (key != ctx->bc_key) {
       ctx->bc_key.clear();
-      if (reserve((void**)&ctx->bc_rec, &ctx->bc_rec_cap, sizeof(uint4) * kRecSlots * s.n_chunks) != cudaSuccess ||
-          reserve((void**)&ctx->bc_map, &ctx->bc_map_cap, sizeof(int) * kBcMapInts * s.n_chunks) != cudaSuccess ||
-          reserve((void**)&ctx->bc_lcol, &ctx->bc_lcol_cap, sizeof(uint16_t) * s.n_slots) != cudaSuccess ||
-          reserve((void**)&ctx->bc_fail, &ctx->bc_fail_cap, sizeof(int)) != cudaSuccess)
-        return fail(ctx, KPM_ENOMEM, "block-cache plan buffers");
+      const bool mem_ok =
+          reserve((void**)&ctx->bc_rec, &ctx->bc_rec_cap, sizeof(uint4) * kRecSlots * s.n_chunks) == cudaSuccess &&
+          (ctx->opt.nranks == 1 ||
+           reserve((void**)&ctx->bc_rec2, &ctx->bc_rec2_cap, sizeof(uint4) * kRecSlots * s.n_chunks) == cudaSuccess) &&
+          reserve((void**)&ctx->bc_map, &ctx->bc_map_cap, sizeof(int) * kBcMapInts * s.n_chunks) == cudaSuccess &&
+          reserve((void**)&ctx->bc_lcol, &ctx->bc_lcol_cap, sizeof(uint16_t) * s.n_slots) == cudaSuccess &&
+          reserve((void**)&ctx->bc_fail, &ctx->bc_fail_cap, sizeof(int)) == cudaSuccess;
+      if (!mem_ok) {  // no room for the plan: the base variant runs (below)
+        cudaGetLastError();
+        ctx->bc_ok = false;
+        ctx->bc_key = key;
+      }
+    }
+    if (key != ctx->bc_key) {
       KPM_CUDA(cudaMemsetAsync(ctx->bc_fail, 0, sizeof(int), ctx->stream));
-      KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->order_list, s.n_chunks, grid, Rk,
-                               variant_wstage(Rk, variant), tl, ctx->bc_rec, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail,
-                               ctx->stream));
+      // one plan per launch list (single rank: the chunk order; several ranks: the edge and the
+      // interior list, whose chunks are disjoint, so they share the lcol array)
+      const bool wst = variant_wstage(Rk, variant);
+      if (ctx->opt.nranks == 1) {
+        KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->order_list, s.n_chunks, grid, Rk, wst, tl,
+                                 ctx->bc_rec, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, ctx->stream));
+      } else {
+        if (ctx->n_edge)
+          KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->edge_list, ctx->n_edge, grid, Rk, wst, tl,
+                                   ctx->bc_rec, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, ctx->stream));
+        if (ctx->n_interior)
+          KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->interior_list, ctx->n_interior, grid, Rk, wst,
+                                   tl, ctx->bc_rec2, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, ctx->stream));
+      }
       int hfail = 0;
       KPM_CUDA(cudaMemcpyAsync(&hfail, ctx->bc_fail, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
       KPM_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -960,6 +983,7 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     sa.chunk_begin = 0;
     sa.chunk_end = ctx->n_edge;
     sa.partials = part;
+    if (bc) sa.rec = ctx->bc_rec;
     if (ctx->fused) {
       // V's halo slots were written by the neighbours' previous edge launch: wait for their flags
       if (m > 0)
@@ -981,6 +1005,7 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
       }
       sa.chunk_list = ctx->interior_list;
       sa.chunk_end = ctx->n_interior;
+      if (bc) sa.rec = ctx->bc_rec2;
       sa.partials = part + grid;
       KPM_CUDA(launch_aug_spmmv(Rk, variant, init, sa, grid, str));
       return KPM_OK;
@@ -996,6 +1021,7 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     }
     sa.chunk_list = ctx->interior_list;
     sa.chunk_end = ctx->n_interior;
+    if (bc) sa.rec = ctx->bc_rec2;
     sa.partials = part + grid;
     KPM_CUDA(launch_aug_spmmv(Rk, variant, init, sa, grid, str));
     return KPM_OK;

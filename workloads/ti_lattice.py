@@ -308,29 +308,36 @@ def chunk_order_yband(lat: Lattice, x0: int, x1: int, band: int, C: int = 32):
     return np.concatenate(order).astype(np.int64)
 
 
-def chunk_order_ylines(lat: Lattice, grid: int, C: int = 32):
+def chunk_order_ylines(lat: Lattice, grid: int, C: int = 32, x0: int = 0, x1: int = None, edges_last: bool = False):
     """Locality hint for kpm_set_chunk_order and the block-cache feed (not method arithmetic):
     list position b + grid*k is CTA b's k-th tile.  In full rounds of `grid` lines, CTA b
     walks one y-line of chunks (x, 0..Ny-1, z-block), all CTAs in step at the same y, so
     consecutive tiles of a CTA share their y-neighbour blocks and the x-neighbour blocks are
     other CTAs' current own blocks (L2 hits).  The lines left over after the last full round
-    follow in storage order (no reuse, perfect balance)."""
+    follow in storage order (no reuse, perfect balance).  Chunk ids are local to the x-slab
+    [x0, x1); with edges_last (several ranks) the slab's first and last x-planes -- the edge
+    chunks, launched separately -- go to the end, so the interior list keeps the rounds."""
     if (4 * lat.nz) % C:
         raise ValueError("needs 8 | Nz so chunks align with z-columns")
     zb = 4 * lat.nz // C
-    n_lines = lat.nx * zb
-    rounds = n_lines // grid
+    nxl = (lat.nx if x1 is None else x1) - x0
+    xs = np.arange(1, nxl - 1) if edges_last and nxl > 2 else np.arange(nxl)
+    lines = (xs[:, None] * zb + np.arange(zb)[None, :]).ravel()  # line id = x * zb + z
+    rounds = len(lines) // grid
     parts = []
     y = np.arange(lat.ny)
     for r in range(rounds):
-        line = r * grid + np.arange(grid)
+        line = lines[r * grid:(r + 1) * grid]
         x, z = line // zb, line % zb
         parts.append(((x[None, :] * lat.ny + y[:, None]) * zb + z[None, :]).ravel())
-    done = rounds * grid
-    if done < n_lines:
-        line = np.arange(done, n_lines)
-        x, z = line // zb, line % zb
+    rest = lines[rounds * grid:]
+    if len(rest):
+        x, z = rest // zb, rest % zb
         parts.append(np.sort(((x[:, None] * lat.ny + y[None, :]) * zb + z[:, None]).ravel()))
+    if edges_last and nxl > 2:
+        ex = np.array([0, nxl - 1])
+        parts.append(np.sort(((ex[:, None, None] * lat.ny + y[None, :, None]) * zb
+                              + np.arange(zb)[None, None, :]).ravel()))
     return np.concatenate(parts).astype(np.int64)
 
 
