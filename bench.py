@@ -312,14 +312,16 @@ def main():
     order = None
     sms = torch.cuda.get_device_properties(local).multi_processor_count
 
-    def yline_order(r):  # the block-cache feed runs 1 CTA per SM at R = 32 and 2 at R = 16 (kernels.cu)
-        return chunk_order_ylines(lat, sms * (2 if r == 16 else 1), x0=x0, x1=x1, edges_last=world > 1)
+    bc_ctas = {16: 2, 32: 1}  # CTAs per SM of the default block-cache feed at each width (kernels.cu)
+
+    def yline_order(r):
+        return chunk_order_ylines(lat, sms * bc_ctas[r], x0=x0, x1=x1, edges_last=world > 1)
 
     use_lines = False
     if args.chunk_order == "auto" and 2 * lat.rows_per_plane * min(R, 32) * 16 > 32e6 and lat.nz % 8 == 0:
         band = max(1, int(16e6 // (2 * 4 * nz * min(R, 32) * 16)))
         order = chunk_order_yband(lat, x0, x1, band)
-    elif args.chunk_order == "auto" and R >= 16 and lat.nz % 8 == 0 and (x1 - x0) * (lat.nz // 8) >= 2 * sms:
+    elif args.chunk_order == "auto" and R in bc_ctas and lat.nz % 8 == 0 and (x1 - x0) * (lat.nz // 8) >= 2 * sms:
         # y-line walks in lock-stepped rounds: consecutive tiles of a CTA share y-neighbour blocks,
         # which the block-cache feed keeps in shared memory
         use_lines = True
@@ -385,7 +387,7 @@ def main():
         by_r = {}
         for r in (1, 2, 4, 8, 16, 32):
             if use_lines:  # only the block-cache widths walk y-lines; the others keep storage order
-                ctx.set_chunk_order(yline_order(r) if r >= 16 else None)
+                ctx.set_chunk_order(yline_order(r) if r in bc_ctas else None)
             ctx.moments(200, r, SEED, want_eta=False)
             ctx.moments(200, r, SEED, want_eta=False)
             sw = ctx.last_timing()[1]

@@ -762,6 +762,9 @@ const Entry kTable[] = {
     KPM_VARIANT(4, 4, 4, kDirect, "direct.lpr4.u4"),
     KPM_VARIANT(4, 4, 8, kDirect, "direct.lpr4.u8"),
     KPM_VARIANT_WR_S(8, 4, 4, 2, "tiled.lpr4.u4.wr.s2"),
+    // block cache at R = 8: -1.4 % power-capped, +3 % at full clock (profiles/r01_bc/bc8.jsonl)
+    {8, "tiled.bc.lpr4.u4.wr", kTiled, false, Variant<8, 4, 4, kTiled, 1, false, 3, true>::launch,
+     Variant<8, 4, 4, kTiled, 1, false, 3, true>::occupancy, 2, 3},
     KPM_VARIANT(8, 4, 4, kTiled, "tiled.lpr4.u4"),
     KPM_VARIANT(8, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kStaged, "staged.lpr8.u4"),

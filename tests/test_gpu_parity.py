@@ -339,7 +339,8 @@ def test_rows_without_diagonal(pkg, R):
 
 @pytest.mark.parametrize("ordered", [False, True])
 @pytest.mark.parametrize("R,dims,name,ctas", [(32, (40, 20, 32), "tiled.bc.lpr8.u4", 1),
-                                             (16, (80, 12, 32), "tiled.bc.lpr4.u4.wr", 2)])
+                                             (16, (80, 12, 32), "tiled.bc.lpr4.u4.wr", 2),
+                                             (8, (120, 8, 32), "tiled.bc.lpr4.u4.wr", 3)])
 def test_block_cache_feed(pkg, monkeypatch, ordered, R, dims, name, ctas):
     """Block-cache feed (tiled.bc): per-CTA pools of 32-row V blocks reused across tiles.  On
     lattices with more z-block lines than CTAs (one lock-stepped round + a storage-order tail),
