@@ -226,8 +226,9 @@ def main():
                     help="bar: (200N)x100x40 weak scaling (= C3 at N=1); C1..C4: the BASELINE.json lattices, "
                          "global size fixed (strong scaling over N); C5: 1800x400x40 slab per GPU (~150 GB HBM), "
                          "M=4000, generated and converted on the GPU (weak scaling)")
-    ap.add_argument("--chunk-order", default="auto", choices=["auto", "none"],
-                    help="auto: y-banded chunk order when the x-neighbour window exceeds ~32 MB, else (1 GPU) y-line walks for the block-cache feed (kpm_set_chunk_order)")
+    ap.add_argument("--chunk-order", default="auto", choices=["auto", "none", "ylines"],
+                    help="auto: y-line walks for the block-cache widths (R = 16, 32) when the slab has enough lines, "
+                         "else a y-banded order when the x-neighbour window exceeds ~32 MB (kpm_set_chunk_order)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-r-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -318,14 +319,16 @@ def main():
         return chunk_order_ylines(lat, sms * bc_ctas[r], x0=x0, x1=x1, edges_last=world > 1)
 
     use_lines = False
-    if args.chunk_order == "auto" and 2 * lat.rows_per_plane * min(R, 32) * 16 > 32e6 and lat.nz % 8 == 0:
-        band = max(1, int(16e6 // (2 * 4 * nz * min(R, 32) * 16)))
-        order = chunk_order_yband(lat, x0, x1, band)
-    elif args.chunk_order == "auto" and R in bc_ctas and lat.nz % 8 == 0 and (x1 - x0) * (lat.nz // 8) >= 2 * sms:
+    lines_ok = R in bc_ctas and lat.nz % 8 == 0 and (x1 - x0) * (lat.nz // 8) >= 2 * sms
+    if (args.chunk_order == "ylines" and R in bc_ctas and lat.nz % 8 == 0) or (args.chunk_order == "auto" and lines_ok):
         # y-line walks in lock-stepped rounds: consecutive tiles of a CTA share y-neighbour blocks,
-        # which the block-cache feed keeps in shared memory
+        # which the block-cache feed keeps in shared memory, and the x-neighbour window a round
+        # keeps in L2 is a few tiles per CTA (C4: 11.04 -> 10.45 ms per sweep vs y-band)
         use_lines = True
         order = yline_order(R)
+    elif args.chunk_order == "auto" and 2 * lat.rows_per_plane * min(R, 32) * 16 > 32e6 and lat.nz % 8 == 0:
+        band = max(1, int(16e6 // (2 * 4 * nz * min(R, 32) * 16)))
+        order = chunk_order_yband(lat, x0, x1, band)
 
     def apply_order():
         if order is not None:
