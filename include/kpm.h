@@ -66,7 +66,7 @@ typedef struct {
                                    is supported                                             */
   int sell_sigma;               /* SELL sorting scope sigma; 0 -> 1 (no sorting). 1 or a
                                    multiple of C                                            */
-  unsigned flags;               /* 0 or KPM_CHECK_HERMITIAN                                 */
+  unsigned flags;               /* 0 or an OR of the KPM_* option flags below               */
 } kpm_options;
 
 /* kpm_options.flags: KPM_CHECK_HERMITIAN makes kpm_set_matrix verify H_ij == conj(H_ji)
@@ -75,6 +75,23 @@ typedef struct {
  * the host; KPM_EINVAL naming the first offending pair otherwise.  The method needs a
  * Hermitian H (the eta -> mu doubling identities). */
 enum { KPM_CHECK_HERMITIAN = 1u };
+/* KPM_DETERMINISTIC: accepted for SURVEY §8(b) compatibility; the library is always
+ *   deterministic (fixed chunk -> CTA map, fixed-order CTA and grid sums, no floating-point
+ *   atomics: bitwise identical moments run to run for a fixed nranks, R and kernel variant).
+ * KPM_TIMING: kpm_moments* record a CUDA event after every sweep (and launch the sweeps one by
+ *   one instead of replaying a CUDA graph); kpm_last_sweep_times returns the per-sweep times.
+ * KPM_VIRTUAL_RANKS: test harness.  nranks contexts on ONE device, one host thread each, form an
+ *   in-process group: nccl_unique_id must point to a kpm_vgroup (kpm_vgroup_create) instead of
+ *   an NCCL id.  Setup collectives and the final eta reduction run on the host through the
+ *   group; the halo exchange is the fused one (peer stores from the edge kernels' epilogue,
+ *   flag epochs) with plain device pointers in place of CUDA IPC mappings.  Every sweep kernel
+ *   and the edge / interior split are the multi-GPU ones, so a single-GPU box can test them. */
+enum { KPM_DETERMINISTIC = 2u, KPM_TIMING = 4u, KPM_VIRTUAL_RANKS = 8u };
+
+typedef struct kpm_vgroup kpm_vgroup; /* opaque in-process rank group (KPM_VIRTUAL_RANKS) */
+/* Create / destroy a group of nranks virtual ranks.  The group must outlive its contexts. */
+kpm_status kpm_vgroup_create(int nranks, kpm_vgroup** out);
+void kpm_vgroup_destroy(kpm_vgroup* group);
 
 typedef struct {
   int64_t n_global;             /* matrix dimension N                               */
@@ -110,7 +127,11 @@ kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, double b);
  * count times the CTAs per SM of the width's kernel; with several ranks the order is split
  * into the edge and the interior list, each keeping its relative order).  The block-cache
  * feed (R = 16, 32) reuses V blocks between a CTA's consecutive tiles, so an order in which
- * they are neighbours (workloads.chunk_order_ylines) cuts its copies by 40 %.
+ * they are neighbours cuts its copies by 40 %.
+ * Without a call (or after order = NULL) the library picks the order itself: for the
+ * block-cache kernels, and for any kernel when the matrix's neighbour window exceeds 32 MB,
+ * the line walk of kpm_plan_chunk_order derived from the matrix's chunk adjacency; otherwise
+ * storage order.  Pass the identity permutation to force storage order.
  * Reset by kpm_set_matrix. */
 kpm_status kpm_set_chunk_order(kpm_ctx* ctx, const int64_t* order, int64_t n);
 
@@ -162,6 +183,12 @@ kpm_status kpm_sweep_kernel(kpm_ctx* ctx, int kind, int R, uint64_t seed, int n_
  * of one main aug_spmmv sweep (the hot kernel); n_sweeps = main sweeps timed. */
 kpm_status kpm_last_timing(const kpm_ctx* ctx, double* total_ms, double* sweep_ms, int* n_sweeps);
 
+/* KPM_TIMING only: the device time (ms, CUDA events on the context's stream) of every sweep of
+ * the last kpm_moments* call, in order (per column block of 32: the init sweep, then the M/2 - 1
+ * main sweeps).  ms = NULL: *n = the number available; otherwise *n is the capacity on entry and
+ * the number written on return.  Without KPM_TIMING, *n = 0. */
+kpm_status kpm_last_sweep_times(const kpm_ctx* ctx, double* ms, int64_t* n);
+
 /* Name of the aug_spmmv kernel variant the last kpm_moments* call ran (feed, lanes per row,
  * unroll), e.g. "staged.lpr16.u4".  "" before the first call.  The
  * environment variable KPM_VARIANT=<i> (read by kpm_create) selects variant i of a block
@@ -191,6 +218,22 @@ kpm_status kpm_get_sell_info(const kpm_ctx* ctx, kpm_sell_info* info);
 kpm_status kpm_export_sell(const kpm_ctx* ctx, double* val, int32_t* col, int64_t* cptr,
                            int32_t* perm, int64_t* halo);
 
+/* The halo exchange plan of this rank (nranks > 1; zero runs on one rank), as kpm_set_matrix
+ * built it (SURVEY §8(b) kpm_export_halo; the halo slot ids themselves: kpm_export_sell `halo`).
+ *   recv: 4 int64 per run (owner rank, first global row, count, first halo slot): halo slots
+ *         [slot, slot + count) receive the owner's global rows [first, first + count).
+ *   send: 4 int64 per run (destination rank, first local position, count, first halo slot in
+ *         the destination's vectors): after every sweep these rows of the new W go there.
+ * recv / send = NULL: only the counts; otherwise *n_recv / *n_send are the capacities (runs),
+ * KPM_EINVAL if too small.  Both counts are set on return. */
+kpm_status kpm_export_halo(const kpm_ctx* ctx, int64_t* n_recv, int64_t* recv, int64_t* n_send, int64_t* send);
+
+/* Row-pair order of every SELL chunk (R18b; csrc/sell_pair.cu): n_chunks int32,
+ * pinfo[c] = m | Ls << 8 -- rows a and a ^ m of chunk c (a with bit lowbit(m) clear) list the
+ * Ls columns they share at entries 1..Ls; 0 = the chunk keeps the R18 order.  The exported
+ * val/col arrays are in this order.  Environment KPM_PAIR=0 (read by kpm_set_matrix) skips it. */
+kpm_status kpm_export_pairs(const kpm_ctx* ctx, int32_t* pinfo);
+
 /* Host-only planning of the halo exchange (no GPU needed; the same code kpm_set_matrix
  * runs).  Row distribution: rank q owns global rows [row_begins[q], row_begins[q+1]).
  * kpm_plan_recv: this rank's receive runs, from its CSR rows (row_ptr, global col) --
@@ -205,6 +248,15 @@ kpm_status kpm_plan_recv(int nranks, const int64_t* row_begins, int rank, const 
                          const int64_t* col, int64_t* n_runs, int64_t* runs);
 kpm_status kpm_plan_send(int64_t row_begin, int64_t row_end, int peer, int64_t n_req, const int64_t* req,
                          int64_t* n_runs, int64_t* runs);
+
+/* Host-only: the library's default chunk order (the locality walk kpm_moments uses when no
+ * kpm_set_chunk_order is given; DESIGN.md §7 "Chunk order").  nbr_ptr (n_chunks+1) / nbr: for
+ * every chunk the chunks all of whose C rows it reads (block neighbours, CSR layout, ids in
+ * [0, n_chunks)); grid: CTAs of the sweep launch (lines per round); skip (NULL or n_chunks
+ * flags): chunks left out of the lines and put last (the edge chunks of a multi-rank split).
+ * order: out, n_chunks int64, a permutation.  KPM_ERANGE for a neighbour id out of range. */
+kpm_status kpm_plan_chunk_order(int64_t n_chunks, const int64_t* nbr_ptr, const int64_t* nbr, int64_t grid,
+                                const int8_t* skip, int64_t* order);
 
 /* Density of states from the moments (north_star item 5; Eq. (2) `DOS`; the
  * "second computationally inexpensive step" of P:258-260).  Host only, no context.

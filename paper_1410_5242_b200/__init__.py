@@ -16,14 +16,15 @@ LIB_PATH = os.path.join(_PKG, "libkpm.so")
 
 KPM_OK, KPM_EINVAL, KPM_ESTATE, KPM_ERANGE, KPM_ENOMEM, KPM_ECUDA, KPM_ENCCL, KPM_EZERONORM, KPM_WDIVERGED = range(9)
 KPM_MEM_HOST, KPM_MEM_DEVICE = 0, 1
-KPM_CHECK_HERMITIAN = 1
+KPM_CHECK_HERMITIAN, KPM_DETERMINISTIC, KPM_TIMING, KPM_VIRTUAL_RANKS = 1, 2, 4, 8
 STATUS_NAMES = ["KPM_OK", "KPM_EINVAL", "KPM_ESTATE", "KPM_ERANGE", "KPM_ENOMEM", "KPM_ECUDA", "KPM_ENCCL",
                 "KPM_EZERONORM", "KPM_WDIVERGED"]
 
 # exported symbols declared in include/kpm.h
-ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_dos", "kpm_export_sell", "kpm_get_sell_info", "kpm_get_unique_id",
-               "kpm_last_error", "kpm_last_kernel", "kpm_last_timing", "kpm_moments", "kpm_moments_stage", "kpm_moments_v0",
-               "kpm_plan_recv", "kpm_plan_send", "kpm_set_chunk_order", "kpm_set_matrix", "kpm_sweep_kernel", "kpm_variant_name"]
+ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_dos", "kpm_export_halo", "kpm_export_pairs", "kpm_export_sell", "kpm_get_sell_info", "kpm_get_unique_id",
+               "kpm_last_error", "kpm_last_kernel", "kpm_last_sweep_times", "kpm_last_timing", "kpm_moments", "kpm_moments_stage", "kpm_moments_v0",
+               "kpm_plan_chunk_order", "kpm_plan_recv", "kpm_plan_send", "kpm_set_chunk_order", "kpm_set_matrix", "kpm_sweep_kernel", "kpm_variant_name", "kpm_vgroup_create",
+               "kpm_vgroup_destroy"]
 
 
 class KpmError(RuntimeError):
@@ -71,6 +72,12 @@ def load_library():
     lib.kpm_last_timing.argtypes = [P, P, P, P]
     lib.kpm_get_sell_info.argtypes = [P, ctypes.POINTER(kpm_sell_info)]
     lib.kpm_export_sell.argtypes = [P, P, P, P, P, P]
+    lib.kpm_export_pairs.argtypes = [P, P]
+    lib.kpm_export_halo.argtypes = [P, P, P, P, P]
+    lib.kpm_last_sweep_times.argtypes = [P, P, P]
+    lib.kpm_vgroup_create.argtypes = [i32, ctypes.POINTER(P)]
+    lib.kpm_vgroup_destroy.argtypes = [P]
+    lib.kpm_vgroup_destroy.restype = None
     lib.kpm_last_error.argtypes = [P]
     lib.kpm_last_error.restype = ctypes.c_char_p
     lib.kpm_last_kernel.argtypes = [P]
@@ -82,10 +89,11 @@ def load_library():
     lib.kpm_dos.argtypes = [i32, P, dbl, dbl, i32, P, i32, P, P]
     lib.kpm_plan_recv.argtypes = [i32, P, i32, P, P, P, P]
     lib.kpm_plan_send.argtypes = [i64, i64, i32, i64, P, P, P]
+    lib.kpm_plan_chunk_order.argtypes = [i64, P, P, i64, P, P]
     lib.kpm_destroy.argtypes = [P]
     lib.kpm_destroy.restype = None
     for name in ABI_SYMBOLS:
-        if name not in ("kpm_last_error", "kpm_last_kernel", "kpm_destroy", "kpm_variant_name"):
+        if name not in ("kpm_last_error", "kpm_last_kernel", "kpm_destroy", "kpm_variant_name", "kpm_vgroup_destroy"):
             getattr(lib, name).restype = i32
     _lib = lib
     return lib
@@ -164,15 +172,50 @@ def plan_send(row_begin, row_end, peer, req):
     return out[: n.value]
 
 
+def plan_chunk_order(nbr_ptr, nbr, grid, skip=None):
+    """kpm_plan_chunk_order: the library's default chunk order from block-neighbour lists."""
+    lib = load_library()
+    nbr_ptr = np.ascontiguousarray(nbr_ptr, dtype=np.int64)
+    nbr = np.ascontiguousarray(nbr, dtype=np.int64)
+    n = len(nbr_ptr) - 1
+    sk = None if skip is None else np.ascontiguousarray(skip, dtype=np.int8)
+    out = np.zeros(max(n, 1), dtype=np.int64)
+    st = lib.kpm_plan_chunk_order(n, _ptr(nbr_ptr), _ptr(nbr) if len(nbr) else None, int(grid), _ptr(sk), _ptr(out))
+    if st != KPM_OK:
+        raise KpmError(st, "kpm_plan_chunk_order")
+    return out[:n]
+
+
+class VirtualGroup:
+    """kpm_vgroup_create: an in-process group of nranks virtual ranks on one device (test harness,
+    KPM_VIRTUAL_RANKS in kpm.h).  Pass it as KpmContext(vgroup=...) from one thread per rank."""
+
+    def __init__(self, nranks):
+        self.lib = load_library()
+        h = ctypes.c_void_p()
+        st = self.lib.kpm_vgroup_create(int(nranks), ctypes.byref(h))
+        if st != KPM_OK:
+            raise KpmError(st, "kpm_vgroup_create")
+        self.h, self.nranks = h, nranks
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.kpm_vgroup_destroy(self.h)
+            self.h = None
+
+
 class KpmContext:
     """One rank's context (kpm_create ... kpm_destroy)."""
 
     def __init__(self, device=0, nranks=1, rank=0, nccl_unique_id=None, cuda_stream=None, sell_C=32, sell_sigma=1,
-                 check_hermitian=False):
+                 check_hermitian=False, flags=0, vgroup=None):
         self.lib = load_library()
         self._uid = None if nccl_unique_id is None else ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
-        opt = kpm_options(device, nranks, rank, ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None,
-                          cuda_stream, sell_C, sell_sigma, KPM_CHECK_HERMITIAN if check_hermitian else 0)
+        uid = ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None
+        flags |= KPM_CHECK_HERMITIAN if check_hermitian else 0
+        if vgroup is not None:
+            uid, flags = vgroup.h, flags | KPM_VIRTUAL_RANKS
+        opt = kpm_options(device, nranks, rank, uid, cuda_stream, sell_C, sell_sigma, flags)
         h = ctypes.c_void_p()
         st = self.lib.kpm_create(ctypes.byref(h), ctypes.byref(opt))
         if st != KPM_OK:
@@ -252,6 +295,23 @@ class KpmContext:
         self._check(self.lib.kpm_last_timing(self.h, ctypes.byref(t), ctypes.byref(s), ctypes.byref(n)))
         return t.value, s.value, n.value
 
+    def sweep_times(self):
+        """kpm_last_sweep_times (KPM_TIMING contexts): per-sweep device ms of the last call."""
+        n = ctypes.c_int64(0)
+        self._check(self.lib.kpm_last_sweep_times(self.h, None, ctypes.byref(n)))
+        out = np.zeros(max(n.value, 1))
+        self._check(self.lib.kpm_last_sweep_times(self.h, _ptr(out), ctypes.byref(n)))
+        return out[: n.value]
+
+    def export_halo(self):
+        """kpm_export_halo: (recv runs (n, 4), send runs (n, 4)) of this rank's exchange plan."""
+        nr, ns = ctypes.c_int64(0), ctypes.c_int64(0)
+        self._check(self.lib.kpm_export_halo(self.h, ctypes.byref(nr), None, ctypes.byref(ns), None))
+        recv = np.zeros((max(nr.value, 1), 4), dtype=np.int64)
+        send = np.zeros((max(ns.value, 1), 4), dtype=np.int64)
+        self._check(self.lib.kpm_export_halo(self.h, ctypes.byref(nr), _ptr(recv), ctypes.byref(ns), _ptr(send)))
+        return recv[: nr.value], send[: ns.value]
+
     def last_kernel(self):
         return self.lib.kpm_last_kernel(self.h).decode()
 
@@ -269,6 +329,12 @@ class KpmContext:
         halo = np.zeros(max(info.n_halo, 1), dtype=np.int64)
         self._check(self.lib.kpm_export_sell(self.h, _ptr(val), _ptr(col), _ptr(cptr), _ptr(perm), _ptr(halo)))
         return dict(val=val, col=col, cptr=cptr, perm=perm, halo=halo[: info.n_halo], n_pad=info.n_pad)
+
+    def export_pairs(self):
+        """kpm_export_pairs: per chunk m | Ls << 8 of the row-pair order (0 = unpaired)."""
+        pinfo = np.zeros(max(self.sell_info().n_chunks, 1), dtype=np.int32)
+        self._check(self.lib.kpm_export_pairs(self.h, _ptr(pinfo)))
+        return pinfo[: self.sell_info().n_chunks]
 
     def close(self):
         if getattr(self, "h", None):

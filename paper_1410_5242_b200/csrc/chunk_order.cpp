@@ -1,0 +1,107 @@
+// Locality order of the SELL chunks, derived inside the library from the matrix itself
+// (DESIGN.md §7 "Chunk order"; the paper's cache-blocking outlook, and the effect of
+// the gathered-vector reuse factor Omega).  Host code, no CUDA: testable on a CPU
+// through kpm_plan_chunk_order (plan_abi.cpp).
+//
+// Chunk b is a *block neighbour* of chunk c when c's entries reference all 32 rows of b (for a
+// stencil such as the TI lattice: the chunks one step away along a periodic/open direction whose
+// sites line up with c's).  The line direction d is the smallest positive chunk offset that at
+// least half of the chunks have as a block neighbour (TI, x slowest: d = Nz/8, one step in y).
+// A line is a maximal chain c, c + d, c + 2d, ... of mutual block neighbours.  Lines of equal
+// length are taken in rounds of G (the sweep grid, one line per CTA, list position b + G k =
+// CTA b's k-th tile), interleaved so that all CTAs are at the same step: consecutive tiles of a
+// CTA then share their line-direction neighbour blocks (the block-cache feed keeps them in shared
+// memory) and the other neighbours are the current tiles of other CTAs (L2 hits).  Lines left
+// over after the last full round, and chunks in no line, follow in storage order.  Chunks with
+// skip[c] != 0 (the edge chunks of a multi-rank split) are kept out of the lines and go last.
+#include <stdint.h>
+
+#include <algorithm>
+#include <map>
+#include <vector>
+
+#include "chunk_order.h"
+
+namespace kpm {
+
+void block_neighbours(int64_t n_chunks, const int* nruns, const int* runs, int max_runs, int C,
+                      std::vector<int64_t>& ptr, std::vector<int64_t>& nbr) {
+  ptr.assign(n_chunks + 1, 0);
+  nbr.clear();
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    for (int k = 0; k < nruns[c]; ++k) {
+      const int64_t first = runs[(c * max_runs + k) * 2], cnt = runs[(c * max_runs + k) * 2 + 1];
+      for (int64_t b = (first + C - 1) / C; (b + 1) * C <= first + cnt; ++b)
+        if (b != c && b < n_chunks) nbr.push_back(b);
+    }
+    ptr[c + 1] = (int64_t)nbr.size();
+  }
+}
+
+std::vector<int64_t> line_order(int64_t n_chunks, const std::vector<int64_t>& ptr, const std::vector<int64_t>& nbr,
+                                int64_t G, const std::vector<char>& skip) {
+  auto in = [&](int64_t c) { return c >= 0 && c < n_chunks && (skip.empty() || !skip[c]); };
+  auto is_nbr = [&](int64_t c, int64_t b) {
+    for (int64_t i = ptr[c]; i < ptr[c + 1]; ++i)
+      if (nbr[i] == b) return true;
+    return false;
+  };
+  // line direction: the smallest positive offset that at least half of the chunks have
+  std::map<int64_t, int64_t> freq;
+  int64_t n_in = 0;
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    if (!in(c)) continue;
+    ++n_in;
+    for (int64_t i = ptr[c]; i < ptr[c + 1]; ++i)
+      if (nbr[i] > c && in(nbr[i])) ++freq[nbr[i] - c];
+  }
+  int64_t d = 0;
+  for (const auto& kv : freq)
+    if (2 * kv.second >= n_in) {
+      d = kv.first;
+      break;
+    }
+  std::vector<int64_t> order;
+  order.reserve(n_chunks);
+  std::vector<char> used(n_chunks, 0);
+  if (d > 0 && G > 0) {
+    auto linked = [&](int64_t c) { return in(c + d) && is_nbr(c, c + d) && is_nbr(c + d, c); };
+    std::vector<std::pair<int64_t, int64_t>> lines;  // (start, length), starts ascending
+    for (int64_t c = 0; c < n_chunks; ++c) {
+      if (!in(c) || (c - d >= 0 && in(c - d) && linked(c - d))) continue;
+      int64_t len = 1;
+      for (int64_t x = c; linked(x); x += d) ++len;
+      lines.push_back({c, len});
+    }
+    // rounds of G lines of equal length (longest first, starts ascending inside a length)
+    std::stable_sort(lines.begin(), lines.end(), [](const auto& a, const auto& b) { return a.second > b.second; });
+    size_t i = 0;
+    while (i < lines.size()) {
+      size_t j = i;
+      while (j < lines.size() && lines[j].second == lines[i].second) ++j;
+      const size_t full = (j - i) / (size_t)G * (size_t)G;
+      for (size_t r = i; r < i + full; r += (size_t)G)
+        for (int64_t step = 0; step < lines[i].second; ++step)
+          for (size_t l = r; l < r + (size_t)G; ++l) {
+            const int64_t c = lines[l].first + step * d;
+            order.push_back(c);
+            used[c] = 1;
+          }
+      i = j;
+    }
+  }
+  for (int64_t c = 0; c < n_chunks; ++c)  // leftover lines and chunks in no line, then skipped ones
+    if (!used[c] && in(c)) order.push_back(c);
+  for (int64_t c = 0; c < n_chunks; ++c)
+    if (!in(c)) order.push_back(c);
+  return order;
+}
+
+int64_t max_block_offset(int64_t n_chunks, const std::vector<int64_t>& ptr, const std::vector<int64_t>& nbr) {
+  int64_t m = 0;
+  for (int64_t c = 0; c < n_chunks; ++c)
+    for (int64_t i = ptr[c]; i < ptr[c + 1]; ++i) m = std::max(m, nbr[i] > c ? nbr[i] - c : c - nbr[i]);
+  return m;
+}
+
+}  // namespace kpm

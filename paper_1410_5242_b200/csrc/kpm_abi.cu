@@ -16,14 +16,46 @@
 #include <nccl.h>
 
 #include <array>
+#include <condition_variable>
 #include <map>
+#include <mutex>
 
 #include "../../include/kpm.h"
+#include "chunk_order.h"
 #include "halo_plan.h"
 #include "kpm_internal.h"
 #include "sell_build.h"
 
 using namespace kpm;
+
+// In-process group of "virtual ranks" (test harness, kpm.h KPM_VIRTUAL_RANKS): nranks contexts on
+// one device, driven by nranks host threads, whose setup collectives and final eta reduction run
+// through this host rendezvous instead of NCCL, and whose fused halo exchange stores into the
+// other contexts' buffers through plain device pointers instead of CUDA IPC mappings.  The sweep
+// kernels, the edge / interior split and the flag-epoch protocol are the multi-GPU ones.
+struct kpm_vgroup {
+  int P = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t gen = 0;
+  std::vector<std::vector<int64_t>> slot, result;
+  // all-gather of variable-length int64 vectors; every rank gets every rank's vector
+  std::vector<std::vector<int64_t>> allgatherv(int rank, const std::vector<int64_t>& mine) {
+    std::unique_lock<std::mutex> lk(mu);
+    slot[rank] = mine;
+    const int64_t g = gen;
+    if (++arrived == P) {
+      result = slot;
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+    return result;
+  }
+};
 
 struct kpm_ctx {
   kpm_options opt{};
@@ -69,6 +101,8 @@ struct kpm_ctx {
 
   // multi-rank (nranks > 1): row distribution, halo exchange plan, NCCL
   ncclComm_t comm = nullptr;
+  kpm_vgroup* vg = nullptr;         // virtual ranks (no NCCL): the in-process group
+  std::vector<int64_t> peer_x0, peer_x1;  // virtual ranks: every rank's X0 / X1 (device pointers)
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_edge = nullptr, ev_halo = nullptr;
   std::vector<int64_t> row_begins;  // nranks+1
@@ -78,8 +112,15 @@ struct kpm_ctx {
   int64_t* interior_list = nullptr; // device: the other chunks
   int64_t n_edge = 0, n_interior = 0;
   std::vector<char> edge_flag;      // host: chunk is an edge chunk
-  std::vector<int64_t> order_h;     // chunk processing order (kpm_set_chunk_order), empty = storage order
-  int64_t* order_list = nullptr;    // device copy for single-rank sweeps
+  std::vector<int64_t> order_h;     // chunk processing order given by kpm_set_chunk_order
+  bool order_user = false;          // order_h is in force (else the library's own choice)
+  int64_t* order_list = nullptr;    // device copy of the installed order for single-rank sweeps
+  int64_t order_id = -3;            // installed order: -1 user, 0 storage, G > 0 line walk for grid G
+  int64_t order_gen = 0;            // bumped by every install (keys of the block-cache plan, CUDA graph)
+  std::map<int64_t, std::vector<int64_t>> auto_order;  // line walk per grid (chunk_order.cpp)
+  int adj_state = 0;                // block-neighbour lists: 0 not built, 1 built, -1 unavailable
+  std::vector<int64_t> adj_ptr, adj;
+  int64_t adj_maxoff = 0;
   int64_t* halo_rows = nullptr;     // device: global id of each halo slot
   // fused halo exchange (peer stores from the sweep epilogue + stream flag ops)
   bool fused = false;               // chosen per set_matrix (env KPM_HALO=nccl|fused)
@@ -104,10 +145,15 @@ struct kpm_ctx {
   uint16_t* bc_lcol = nullptr;
   int* bc_fail = nullptr;
   size_t bc_rec_cap = 0, bc_map_cap = 0, bc_lcol_cap = 0, bc_fail_cap = 0;
-  std::vector<int64_t> bc_key;      // (R, grid, matrix_gen, stages) the buffers were built for
+  std::vector<int64_t> bc_key;      // (R, grid, matrix_gen, stages, ...) the buffers were built for
+  int chosen[6] = {0, 0, 0, 0, 0, 0};  // per log2(R): selected variant (select_variant) ...
+  int64_t chosen_gen[6] = {-1, -1, -1, -1, -1, -1};  // ... for this matrix_gen ...
+  int chosen_ovr[6] = {-2, -2, -2, -2, -2, -2};      // ... and this KPM_VARIANT override
   bool bc_ok = false;
   double last_total_ms = 0.0, last_sweep_ms = 0.0;
   int last_n_sweeps = 0;
+  std::vector<cudaEvent_t> sweep_ev;   // KPM_TIMING: one event after every sweep of a block
+  std::vector<double> sweep_times;     // KPM_TIMING: per-sweep ms of the last call (all blocks)
 };
 
 static std::string g_create_err;
@@ -161,7 +207,12 @@ extern "C" kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt) {
     g_create_err = "unsupported SELL parameters (C must be 32, sigma 1 or a multiple of 32)";
     return KPM_EINVAL;
   }
-  if (opt->flags & ~(unsigned)KPM_CHECK_HERMITIAN) {
+  const bool virt = (opt->flags & KPM_VIRTUAL_RANKS) != 0;
+  if (virt && (!opt->nccl_unique_id || static_cast<const kpm_vgroup*>(opt->nccl_unique_id)->P != opt->nranks)) {
+    g_create_err = "KPM_VIRTUAL_RANKS needs nccl_unique_id = a kpm_vgroup of nranks ranks";
+    return KPM_EINVAL;
+  }
+  if (opt->flags & ~(unsigned)(KPM_CHECK_HERMITIAN | KPM_DETERMINISTIC | KPM_TIMING | KPM_VIRTUAL_RANKS)) {
     g_create_err = "unknown kpm_options.flags bits";
     return KPM_EINVAL;
   }
@@ -185,8 +236,13 @@ extern "C" kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt) {
   }
   if (opt->nranks > 1) {
     ncclUniqueId id;
-    std::memcpy(&id, opt->nccl_unique_id, sizeof(id));
-    ncclResult_t r = ncclCommInitRank(&ctx->comm, opt->nranks, id, opt->rank);
+    ncclResult_t r = ncclSuccess;
+    if (virt) {
+      ctx->vg = static_cast<kpm_vgroup*>(const_cast<void*>(opt->nccl_unique_id));
+    } else {
+      std::memcpy(&id, opt->nccl_unique_id, sizeof(id));
+      r = ncclCommInitRank(&ctx->comm, opt->nranks, id, opt->rank);
+    }
     if (r == ncclSuccess) {
       e = cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_edge, cudaEventDisableTiming);
@@ -213,6 +269,7 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->opt.device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
   free_sell(ctx->sell);
   cudaFree(ctx->X0);
   cudaFree(ctx->X1);
@@ -228,6 +285,7 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   if (ctx->h_eta) cudaFreeHost(ctx->h_eta);
   for (int i = 0; i < 4; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  for (cudaEvent_t e : ctx->sweep_ev) cudaEventDestroy(e);
   cudaFree(ctx->edge_list);
   cudaFree(ctx->interior_list);
   cudaFree(ctx->halo_rows);
@@ -247,6 +305,17 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   delete ctx;
 }
 
+extern "C" kpm_status kpm_vgroup_create(int nranks, kpm_vgroup** out) {
+  if (!out || nranks < 1) return KPM_EINVAL;
+  kpm_vgroup* g = new kpm_vgroup();
+  g->P = nranks;
+  g->slot.resize(nranks);
+  *out = g;
+  return KPM_OK;
+}
+
+extern "C" void kpm_vgroup_destroy(kpm_vgroup* g) { delete g; }
+
 extern "C" kpm_status kpm_get_unique_id(void* out) {
   if (!out) return KPM_EINVAL;
   ncclUniqueId id;
@@ -258,6 +327,11 @@ extern "C" kpm_status kpm_get_unique_id(void* out) {
 // Small host<->device collective helpers for the setup (synchronous, compute stream).
 static kpm_status allgather_i64(kpm_ctx* ctx, const std::vector<int64_t>& mine, std::vector<int64_t>& all) {
   const size_t n = mine.size(), P = (size_t)ctx->opt.nranks;
+  if (ctx->vg) {
+    all.clear();
+    for (const auto& v : ctx->vg->allgatherv(ctx->opt.rank, mine)) all.insert(all.end(), v.begin(), v.end());
+    return KPM_OK;
+  }
   int64_t* d = nullptr;
   KPM_CUDA(cudaMalloc(&d, sizeof(int64_t) * n * (P + 1)));
   KPM_CUDA(cudaMemcpy(d, mine.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
@@ -266,6 +340,23 @@ static kpm_status allgather_i64(kpm_ctx* ctx, const std::vector<int64_t>& mine, 
   KPM_CUDA(cudaMemcpyAsync(all.data(), d + n, sizeof(int64_t) * n * P, cudaMemcpyDeviceToHost, ctx->stream));
   KPM_CUDA(cudaStreamSynchronize(ctx->stream));
   KPM_CUDA(cudaFree(d));
+  return KPM_OK;
+}
+
+// Multi-rank: every rank learns whether any rank failed a local step (allocation, validation,
+// plan) before the next collective, so that no rank is left waiting in NCCL or on a halo flag.
+// Returns this rank's status, or KPM_EINVAL/the other rank's status if only another rank failed.
+static kpm_status agree(kpm_ctx* ctx, kpm_status mine) {
+  if (ctx->opt.nranks == 1) return mine;
+  std::vector<int64_t> all;
+  const std::string saved = ctx->err;
+  const kpm_status st = allgather_i64(ctx, {(int64_t)mine}, all);
+  if (st != KPM_OK) return st;
+  ctx->err = saved;
+  if (mine != KPM_OK) return mine;
+  for (size_t q = 0; q < all.size(); ++q)
+    if (all[q] != KPM_OK && all[q] != KPM_WDIVERGED)
+      return fail(ctx, (kpm_status)all[q], "rank " + std::to_string(q) + " failed with status " + std::to_string(all[q]));
   return KPM_OK;
 }
 
@@ -281,6 +372,7 @@ static void free_sell(DevSell& s) {
   cudaFree(s.lcol);
   cudaFree(s.nruns);
   cudaFree(s.runs);
+  cudaFree(s.pinfo);
   for (int i = 0; i < 12; ++i) cudaFree(s.rec[i]);
   s = DevSell();
 }
@@ -291,6 +383,7 @@ static void reset_sell(DevSell& s) {
   k.val = s.val, k.col = s.col, k.cptr = s.cptr, k.perm_buf = s.perm_buf, k.lcol = s.lcol, k.nruns = s.nruns, k.runs = s.runs;
   k.val_cap = s.val_cap, k.col_cap = s.col_cap, k.cptr_cap = s.cptr_cap, k.perm_cap = s.perm_cap;
   k.lcol_cap = s.lcol_cap, k.nruns_cap = s.nruns_cap, k.runs_cap = s.runs_cap;
+  k.pinfo = s.pinfo, k.pinfo_cap = s.pinfo_cap;
   for (int i = 0; i < 12; ++i) {
     k.rec[i] = s.rec[i];
     k.rec_cap[i] = s.rec_cap[i];
@@ -319,6 +412,18 @@ static kpm_status plan_exchange(kpm_ctx* ctx, const std::vector<int64_t>& halo, 
   int64_t tot_out = 0, tot_in = 0;
   for (int q = 0; q < P; ++q) tot_out += all[(size_t)me * P + q];
   for (int p = 0; p < P; ++p) tot_in += all[(size_t)p * P + me];
+  std::vector<int64_t> incoming(tot_in);
+  if (ctx->vg) {  // virtual ranks: every rank sees every rank's requests, keeps those sent to it
+    std::vector<int64_t> flat;
+    for (int q = 0; q < P; ++q) flat.insert(flat.end(), req[q].begin(), req[q].end());
+    const auto got = ctx->vg->allgatherv(me, flat);
+    int64_t in = 0;
+    for (int p = 0; p < P; ++p) {
+      int64_t o = 0;
+      for (int q = 0; q < me; ++q) o += all[(size_t)p * P + q];
+      for (int64_t i = 0; i < all[(size_t)p * P + me]; ++i) incoming[in++] = got[p][o + i];
+    }
+  } else {
   int64_t* dbuf = nullptr;
   KPM_CUDA(cudaMalloc(&dbuf, sizeof(int64_t) * std::max<int64_t>(1, tot_out + tot_in)));
   std::vector<int64_t> flat;
@@ -337,12 +442,12 @@ static kpm_status plan_exchange(kpm_ctx* ctx, const std::vector<int64_t>& halo, 
     in += n;
   }
   KPM_NCCL(ncclGroupEnd());
-  std::vector<int64_t> incoming(tot_in);
   if (tot_in)
     KPM_CUDA(cudaMemcpyAsync(incoming.data(), dbuf + tot_out, sizeof(int64_t) * tot_in, cudaMemcpyDeviceToHost,
                              ctx->stream));
   KPM_CUDA(cudaStreamSynchronize(ctx->stream));
   KPM_CUDA(cudaFree(dbuf));
+  }
   int64_t off = 0;
   for (int p = 0; p < P; ++p) {
     const int64_t n = all[(size_t)p * P + me];
@@ -370,34 +475,72 @@ static kpm_status plan_exchange(kpm_ctx* ctx, const std::vector<int64_t>& halo, 
   return KPM_OK;
 }
 
-// Work lists of the sweep launches in the current chunk order: single rank -> order_list (or
-// the plain range when no order is set); multi-rank -> edge and interior lists, each in order.
-static kpm_status apply_order(kpm_ctx* ctx) {
+// Install a chunk order (empty = storage order) as the work lists of the sweep launches: single
+// rank -> order_list (NULL for storage order); multi-rank -> the edge and the interior list, each
+// in that order.  id names it (see kpm_ctx::order_id) so that repeated requests are free.
+static kpm_status install_order(kpm_ctx* ctx, const std::vector<int64_t>& ord_in, int64_t id) {
+  if (id == ctx->order_id) return KPM_OK;
   const int64_t n = ctx->sell.n_chunks;
-  ++ctx->matrix_gen;
-  std::vector<int64_t> ord = ctx->order_h;
-  if (ord.empty()) {
-    ord.resize(n);
-    for (int64_t c = 0; c < n; ++c) ord[c] = c;
-  }
   cudaFree(ctx->order_list);
   ctx->order_list = nullptr;
+  ctx->order_id = -3;
+  ++ctx->order_gen;
   if (ctx->opt.nranks == 1) {
-    if (!ctx->order_h.empty()) {
+    if (!ord_in.empty()) {
       KPM_CUDA(cudaMalloc(&ctx->order_list, sizeof(int64_t) * n));
-      KPM_CUDA(cudaMemcpy(ctx->order_list, ord.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+      KPM_CUDA(cudaMemcpy(ctx->order_list, ord_in.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
     }
+    ctx->order_id = id;
     return KPM_OK;
   }
   std::vector<int64_t> edge, interior;
-  for (int64_t c : ord) (ctx->edge_flag[c] ? edge : interior).push_back(c);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t c = ord_in.empty() ? i : ord_in[i];
+    (ctx->edge_flag[c] ? edge : interior).push_back(c);
+  }
   ctx->n_edge = (int64_t)edge.size();
   ctx->n_interior = (int64_t)interior.size();
   if (!edge.empty())
     KPM_CUDA(cudaMemcpy(ctx->edge_list, edge.data(), sizeof(int64_t) * edge.size(), cudaMemcpyHostToDevice));
   if (!interior.empty())
     KPM_CUDA(cudaMemcpy(ctx->interior_list, interior.data(), sizeof(int64_t) * interior.size(), cudaMemcpyHostToDevice));
+  ctx->order_id = id;
   return KPM_OK;
+}
+
+// Block-neighbour lists of the chunks (chunk_order.cpp), from the tiled feed's run lists.
+static kpm_status ensure_adjacency(kpm_ctx* ctx) {
+  if (ctx->adj_state != 0) return KPM_OK;
+  const DevSell& s = ctx->sell;
+  ctx->adj_state = -1;
+  if (!s.tiles_ok || s.n_chunks < 1) return KPM_OK;
+  std::vector<int> nr(s.n_chunks), rr((size_t)2 * kMaxRuns * s.n_chunks);
+  KPM_CUDA(cudaMemcpy(nr.data(), s.nruns, sizeof(int) * nr.size(), cudaMemcpyDeviceToHost));
+  KPM_CUDA(cudaMemcpy(rr.data(), s.runs, sizeof(int) * rr.size(), cudaMemcpyDeviceToHost));
+  block_neighbours(s.n_chunks, nr.data(), rr.data(), kMaxRuns, kC, ctx->adj_ptr, ctx->adj);
+  ctx->adj_maxoff = max_block_offset(s.n_chunks, ctx->adj_ptr, ctx->adj);
+  ctx->adj_state = 1;
+  return KPM_OK;
+}
+
+// The chunk order a launch of `grid` CTAs runs: the caller's (kpm_set_chunk_order), else the
+// line walk when want_lines (block-cache kernels; any kernel whose storage-order neighbour
+// window exceeds 32 MB), else storage order.
+static kpm_status ensure_order(kpm_ctx* ctx, int64_t grid, bool bc_kernel, int Rk) {
+  if (ctx->order_user) return install_order(ctx, ctx->order_h, -1);
+  kpm_status st = ensure_adjacency(ctx);
+  if (st != KPM_OK) return st;
+  const bool big_window = ctx->adj_state == 1 && (double)ctx->adj_maxoff * kC * Rk * 16.0 > 32e6;
+  if (ctx->adj_state == 1 && (bc_kernel || big_window) && env_int("KPM_AUTO_ORDER", 1)) {
+    std::vector<int64_t>& o = ctx->auto_order[grid];
+    if (o.empty()) {
+      std::vector<char> skip;
+      if (ctx->opt.nranks > 1) skip = ctx->edge_flag;
+      o = line_order(ctx->sell.n_chunks, ctx->adj_ptr, ctx->adj, grid, skip);
+    }
+    return install_order(ctx, o, grid);
+  }
+  return install_order(ctx, {}, 0);
 }
 
 extern "C" kpm_status kpm_set_chunk_order(kpm_ctx* ctx, const int64_t* order, int64_t n) {
@@ -405,23 +548,35 @@ extern "C" kpm_status kpm_set_chunk_order(kpm_ctx* ctx, const int64_t* order, in
   if (ctx->sticky) return fail(ctx, KPM_ESTATE, "context has a sticky CUDA/NCCL error: " + ctx->err);
   if (!ctx->have_matrix) return fail(ctx, KPM_ESTATE, "kpm_set_matrix has not been called");
   KPM_CUDA(cudaSetDevice(ctx->opt.device));
-  if (!order) {
-    ctx->order_h.clear();
-    return apply_order(ctx);
+  if (order) {
+    if (n != ctx->sell.n_chunks) return fail(ctx, KPM_EINVAL, "order must list every chunk once");
+    std::vector<char> seen(n, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (order[i] < 0 || order[i] >= n || seen[order[i]]) return fail(ctx, KPM_EINVAL, "order is not a permutation");
+      seen[order[i]] = 1;
+    }
   }
-  if (n != ctx->sell.n_chunks) return fail(ctx, KPM_EINVAL, "order must list every chunk once");
-  std::vector<char> seen(n, 0);
-  for (int64_t i = 0; i < n; ++i) {
-    if (order[i] < 0 || order[i] >= n || seen[order[i]]) return fail(ctx, KPM_EINVAL, "order is not a permutation");
-    seen[order[i]] = 1;
-  }
-  ctx->order_h.assign(order, order + n);
-  return apply_order(ctx);
+  ctx->order_user = order != nullptr;
+  ctx->order_h.assign(order, order + (order ? n : 0));
+  ctx->order_id = -3;  // (re)installed by the next kpm_moments*
+  ++ctx->matrix_gen;   // the kernel choice and its block-cache plan depend on the order
+  return KPM_OK;
 }
 
 // After a sweep: owners' new rows of X -> the neighbours' halo slots of X (grouped NCCL P2P).
 static kpm_status exchange_halo(kpm_ctx* ctx, double2* X, int Rk, cudaStream_t s) {
   const int64_t n_pad = ctx->sell.n_pad;
+  if (ctx->vg) {  // virtual ranks: pull the halo rows from the owners' buffers (sigma = 1 positions)
+    KPM_CUDA(cudaStreamSynchronize(s));
+    const auto xs = ctx->vg->allgatherv(ctx->opt.rank, {(int64_t)X});  // everyone's rows are final
+    for (const RecvRun& r : ctx->recv_runs) {
+      const double2* src = reinterpret_cast<const double2*>(xs[r.peer][0]) + (r.gfirst - ctx->row_begins[r.peer]) * Rk;
+      KPM_CUDA(cudaMemcpyAsync(X + (n_pad + r.slot) * Rk, src, sizeof(double2) * r.count * Rk, cudaMemcpyDeviceToDevice, s));
+    }
+    KPM_CUDA(cudaStreamSynchronize(s));
+    ctx->vg->allgatherv(ctx->opt.rank, {});  // nobody overwrites its rows before all copies are done
+    return KPM_OK;
+  }
   KPM_NCCL(ncclGroupStart());
   for (const SendRun& r : ctx->send_runs)
     KPM_NCCL(ncclSend(X + r.pos * Rk, (size_t)r.count * Rk * 2, ncclDouble, r.peer, ctx->comm, s));
@@ -475,7 +630,12 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
     }
     std::string herr;
     const int hs = check_hermitian(rp, col, val, n_loc, H->row_begin, H->row_end, H->n_global, 1e-12, herr);
-    if (hs) return fail(ctx, (kpm_status)hs, herr);
+    if (hs) fail(ctx, (kpm_status)hs, herr);
+    kpm_status ag = agree(ctx, (kpm_status)hs);
+    if (ag != KPM_OK) return ag;
+  } else if (ctx->opt.nranks > 1) {
+    kpm_status ag = agree(ctx, KPM_OK);  // keep the collective sequence identical on every rank
+    if (ag != KPM_OK) return ag;
   }
 
   reset_sell(ctx->sell);
@@ -484,144 +644,166 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
   std::vector<int64_t> halo;       // global ids of the halo slots
   std::vector<int32_t> perm_h;     // host perm (empty = identity)
   std::vector<char> reads_halo;    // per chunk, multi-rank planning
+  auto build = [&]() -> kpm_status {
 
-  // sigma = 1 builds on the device (sell_device.cu); a host CSR is staged to the device first
-  // (one H2D copy, then the same kernels), unless that does not fit or KPM_HOST_BUILD=1.
-  bool dev_build = ctx->opt.sell_sigma == 1 && env_int("KPM_HOST_BUILD", 0) == 0;
-  int64_t* st_rp = nullptr;
-  int64_t* st_col = nullptr;
-  double2* st_val = nullptr;
-  if (dev_build && H->mem == KPM_MEM_HOST) {
-    const int64_t nnz = H->row_ptr[n_loc];
-    if (H->row_ptr[0] != 0 || nnz < 0) return fail(ctx, KPM_EINVAL, "malformed row_ptr");
-    if (reserve((void**)&ctx->stage_rp, &ctx->stage_rp_cap, sizeof(int64_t) * (n_loc + 1)) != cudaSuccess ||
-        reserve((void**)&ctx->stage_col, &ctx->stage_col_cap, sizeof(int64_t) * nnz) != cudaSuccess ||
-        reserve((void**)&ctx->stage_val, &ctx->stage_val_cap, sizeof(double2) * nnz) != cudaSuccess) {
-      cudaGetLastError();
-      dev_build = false;  // not enough device memory for the staging copy: host build
-    } else {
-      st_rp = ctx->stage_rp;
-      st_col = ctx->stage_col;
-      st_val = ctx->stage_val;
-      KPM_CUDA(cudaMemcpyAsync(st_rp, H->row_ptr, sizeof(int64_t) * (n_loc + 1), cudaMemcpyHostToDevice, ctx->stream));
-      KPM_CUDA(cudaMemcpyAsync(st_col, H->col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, ctx->stream));
-      KPM_CUDA(cudaMemcpyAsync(st_val, H->val, sizeof(double2) * nnz, cudaMemcpyHostToDevice, ctx->stream));
-    }
-  }
-  if (dev_build) {
-    // device build: the CSR never leaves the GPU
-    DeviceBuild db;
-    std::string berr;
-    const bool staged = st_rp != nullptr;
-    const int st = build_sell_device(staged ? st_rp : H->row_ptr, staged ? st_col : H->col,
-                                     staged ? st_val : reinterpret_cast<const double2*>(H->val), n_loc,
-                                     H->row_begin, H->row_end, H->n_global, d, db, ctx->build_ws, berr, ctx->stream);
-    if (staged) cudaStreamSynchronize(ctx->stream);
-    if (st) {
-      reset_sell(ctx->sell);
-      cudaGetLastError();
-      if (st == 5) {
-        ctx->sticky = true;
-        return fail(ctx, KPM_ECUDA, berr);
+    // sigma = 1 builds on the device (sell_device.cu); a host CSR is staged to the device first
+    // (one H2D copy, then the same kernels), unless that does not fit or KPM_HOST_BUILD=1.
+    bool dev_build = ctx->opt.sell_sigma == 1 && env_int("KPM_HOST_BUILD", 0) == 0;
+    int64_t* st_rp = nullptr;
+    int64_t* st_col = nullptr;
+    double2* st_val = nullptr;
+    if (dev_build && H->mem == KPM_MEM_HOST) {
+      const int64_t nnz = H->row_ptr[n_loc];
+      if (H->row_ptr[0] != 0 || nnz < 0) return fail(ctx, KPM_EINVAL, "malformed row_ptr");
+      if (reserve((void**)&ctx->stage_rp, &ctx->stage_rp_cap, sizeof(int64_t) * (n_loc + 1)) != cudaSuccess ||
+          reserve((void**)&ctx->stage_col, &ctx->stage_col_cap, sizeof(int64_t) * nnz) != cudaSuccess ||
+          reserve((void**)&ctx->stage_val, &ctx->stage_val_cap, sizeof(double2) * nnz) != cudaSuccess) {
+        cudaGetLastError();
+        dev_build = false;  // not enough device memory for the staging copy: host build
+      } else {
+        st_rp = ctx->stage_rp;
+        st_col = ctx->stage_col;
+        st_val = ctx->stage_val;
+        KPM_CUDA(cudaMemcpyAsync(st_rp, H->row_ptr, sizeof(int64_t) * (n_loc + 1), cudaMemcpyHostToDevice, ctx->stream));
+        KPM_CUDA(cudaMemcpyAsync(st_col, H->col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+        KPM_CUDA(cudaMemcpyAsync(st_val, H->val, sizeof(double2) * nnz, cudaMemcpyHostToDevice, ctx->stream));
       }
-      return fail(ctx, (kpm_status)st, berr);
     }
-    halo = std::move(db.halo);
-    reads_halo = std::move(db.reads_halo);
-    ctx->cptr_h = std::move(db.cptr);
-  } else {
-    // host build (device input is staged through the host)
-    std::vector<int64_t> rp_h, col_h;
-    std::vector<double> val_h;
-    const int64_t* rp = H->row_ptr;
-    const int64_t* col = H->col;
-    const double* val = H->val;
-    if (H->mem == KPM_MEM_DEVICE) {
-      rp_h.resize(n_loc + 1);
-      KPM_CUDA(cudaMemcpy(rp_h.data(), H->row_ptr, sizeof(int64_t) * (n_loc + 1), cudaMemcpyDeviceToHost));
-      const int64_t nnz = rp_h[n_loc];
-      if (nnz < 0) return fail(ctx, KPM_EINVAL, "malformed row_ptr");
-      col_h.resize(nnz);
-      val_h.resize(2 * nnz);
-      KPM_CUDA(cudaMemcpy(col_h.data(), H->col, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
-      KPM_CUDA(cudaMemcpy(val_h.data(), H->val, sizeof(double) * 2 * nnz, cudaMemcpyDeviceToHost));
-      rp = rp_h.data();
-      col = col_h.data();
-      val = val_h.data();
-    }
-    if (rp[0] != 0) return fail(ctx, KPM_EINVAL, "row_ptr[0] != 0");
-    for (int64_t i = 0; i < n_loc; ++i)
-      if (rp[i + 1] < rp[i]) return fail(ctx, KPM_EINVAL, "row_ptr not non-decreasing");
-    const int64_t nnz = rp[n_loc];
-    for (int64_t k = 0; k < nnz; ++k) {
-      if (col[k] < 0 || col[k] >= H->n_global) return fail(ctx, KPM_ERANGE, "column outside [0, n_global)");
-      if (!std::isfinite(val[2 * k]) || !std::isfinite(val[2 * k + 1])) return fail(ctx, KPM_EINVAL, "non-finite value");
-    }
-    HostSell hs;
-    std::string berr;
-    int st = build_sell_host(rp, col, val, n_loc, H->row_begin, H->row_end, ctx->opt.sell_C, ctx->opt.sell_sigma, hs,
-                             berr);
-    if (st) return fail(ctx, (kpm_status)st, berr);
-    d.n_loc = hs.n_loc;
-    d.n_pad = hs.n_pad;
-    d.n_chunks = hs.n_chunks;
-    d.n_slots = hs.cptr[hs.n_chunks];
-    d.n_halo = hs.n_halo;
-    d.max_width = 0;
-    for (int64_t c = 0; c < hs.n_chunks; ++c) d.max_width = std::max(d.max_width, (hs.cptr[c + 1] - hs.cptr[c]) / hs.C);
-    cudaError_t e = reserve((void**)&d.val, &d.val_cap, sizeof(double2) * d.n_slots);
-    if (e == cudaSuccess) e = reserve((void**)&d.col, &d.col_cap, sizeof(int) * d.n_slots);
-    if (e == cudaSuccess) e = reserve((void**)&d.cptr, &d.cptr_cap, sizeof(int64_t) * (d.n_chunks + 1));
-    if (e == cudaSuccess && hs.sigma > 1) e = reserve((void**)&d.perm_buf, &d.perm_cap, sizeof(int) * d.n_loc);
-    if (e == cudaSuccess && hs.sigma > 1) d.perm = d.perm_buf;
-    if (e != cudaSuccess) {
-      reset_sell(ctx->sell);
-      cudaGetLastError();
-      return fail(ctx, KPM_ENOMEM, std::string("device allocation for the matrix failed: ") + cudaGetErrorString(e));
-    }
-    KPM_CUDA(cudaMemcpy(d.val, hs.val.data(), sizeof(double2) * d.n_slots, cudaMemcpyHostToDevice));
-    KPM_CUDA(cudaMemcpy(d.col, hs.col.data(), sizeof(int) * d.n_slots, cudaMemcpyHostToDevice));
-    KPM_CUDA(cudaMemcpy(d.cptr, hs.cptr.data(), sizeof(int64_t) * (d.n_chunks + 1), cudaMemcpyHostToDevice));
-    if (hs.sigma > 1) {
-      KPM_CUDA(cudaMemcpy(d.perm, hs.perm.data(), sizeof(int) * d.n_loc, cudaMemcpyHostToDevice));
-      perm_h = hs.perm;
-    }
-    // gather plan of the tiled feed: lcol + fixed-capacity run lists (records per R on use)
-    HostTiles t;
-    build_tiles_host(hs, t);
-    d.tiles_ok = t.ok && t.max_runs <= kMaxRuns;
-    d.max_other = t.max_other;
-    d.max_runs = t.max_runs;
-    if (d.tiles_ok) {
-      std::vector<int> nr(d.n_chunks), rr((size_t)2 * kMaxRuns * d.n_chunks, 0);
-      for (int64_t c = 0; c < d.n_chunks; ++c) {
-        nr[c] = (int)(t.run_ptr[c + 1] - t.run_ptr[c]);
-        for (int64_t k = t.run_ptr[c]; k < t.run_ptr[c + 1]; ++k) {
-          rr[c * 2 * kMaxRuns + 2 * (k - t.run_ptr[c])] = t.runs[2 * k];
-          rr[c * 2 * kMaxRuns + 2 * (k - t.run_ptr[c]) + 1] = t.runs[2 * k + 1];
+    if (dev_build) {
+      // device build: the CSR never leaves the GPU
+      DeviceBuild db;
+      std::string berr;
+      const bool staged = st_rp != nullptr;
+      const int st = build_sell_device(staged ? st_rp : H->row_ptr, staged ? st_col : H->col,
+                                       staged ? st_val : reinterpret_cast<const double2*>(H->val), n_loc,
+                                       H->row_begin, H->row_end, H->n_global, d, db, ctx->build_ws, berr, ctx->stream);
+      if (staged) cudaStreamSynchronize(ctx->stream);
+      if (st) {
+        reset_sell(ctx->sell);
+        cudaGetLastError();
+        if (st == 5) {
+          ctx->sticky = true;
+          return fail(ctx, KPM_ECUDA, berr);
+        }
+        return fail(ctx, (kpm_status)st, berr);
+      }
+      halo = std::move(db.halo);
+      reads_halo = std::move(db.reads_halo);
+      ctx->cptr_h = std::move(db.cptr);
+    } else {
+      // host build (device input is staged through the host)
+      std::vector<int64_t> rp_h, col_h;
+      std::vector<double> val_h;
+      const int64_t* rp = H->row_ptr;
+      const int64_t* col = H->col;
+      const double* val = H->val;
+      if (H->mem == KPM_MEM_DEVICE) {
+        rp_h.resize(n_loc + 1);
+        KPM_CUDA(cudaMemcpy(rp_h.data(), H->row_ptr, sizeof(int64_t) * (n_loc + 1), cudaMemcpyDeviceToHost));
+        const int64_t nnz = rp_h[n_loc];
+        if (nnz < 0) return fail(ctx, KPM_EINVAL, "malformed row_ptr");
+        col_h.resize(nnz);
+        val_h.resize(2 * nnz);
+        KPM_CUDA(cudaMemcpy(col_h.data(), H->col, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
+        KPM_CUDA(cudaMemcpy(val_h.data(), H->val, sizeof(double) * 2 * nnz, cudaMemcpyDeviceToHost));
+        rp = rp_h.data();
+        col = col_h.data();
+        val = val_h.data();
+      }
+      if (rp[0] != 0) return fail(ctx, KPM_EINVAL, "row_ptr[0] != 0");
+      for (int64_t i = 0; i < n_loc; ++i)
+        if (rp[i + 1] < rp[i]) return fail(ctx, KPM_EINVAL, "row_ptr not non-decreasing");
+      const int64_t nnz = rp[n_loc];
+      for (int64_t k = 0; k < nnz; ++k) {
+        if (col[k] < 0 || col[k] >= H->n_global) return fail(ctx, KPM_ERANGE, "column outside [0, n_global)");
+        if (!std::isfinite(val[2 * k]) || !std::isfinite(val[2 * k + 1])) return fail(ctx, KPM_EINVAL, "non-finite value");
+      }
+      HostSell hs;
+      std::string berr;
+      int st = build_sell_host(rp, col, val, n_loc, H->row_begin, H->row_end, ctx->opt.sell_C, ctx->opt.sell_sigma, hs,
+                               berr);
+      if (st) return fail(ctx, (kpm_status)st, berr);
+      d.n_loc = hs.n_loc;
+      d.n_pad = hs.n_pad;
+      d.n_chunks = hs.n_chunks;
+      d.n_slots = hs.cptr[hs.n_chunks];
+      d.n_halo = hs.n_halo;
+      d.max_width = 0;
+      for (int64_t c = 0; c < hs.n_chunks; ++c) d.max_width = std::max(d.max_width, (hs.cptr[c + 1] - hs.cptr[c]) / hs.C);
+      cudaError_t e = reserve((void**)&d.val, &d.val_cap, sizeof(double2) * d.n_slots);
+      if (e == cudaSuccess) e = reserve((void**)&d.col, &d.col_cap, sizeof(int) * d.n_slots);
+      if (e == cudaSuccess) e = reserve((void**)&d.cptr, &d.cptr_cap, sizeof(int64_t) * (d.n_chunks + 1));
+      if (e == cudaSuccess && hs.sigma > 1) e = reserve((void**)&d.perm_buf, &d.perm_cap, sizeof(int) * d.n_loc);
+      if (e == cudaSuccess && hs.sigma > 1) d.perm = d.perm_buf;
+      if (e != cudaSuccess) {
+        reset_sell(ctx->sell);
+        cudaGetLastError();
+        return fail(ctx, KPM_ENOMEM, std::string("device allocation for the matrix failed: ") + cudaGetErrorString(e));
+      }
+      KPM_CUDA(cudaMemcpy(d.val, hs.val.data(), sizeof(double2) * d.n_slots, cudaMemcpyHostToDevice));
+      KPM_CUDA(cudaMemcpy(d.col, hs.col.data(), sizeof(int) * d.n_slots, cudaMemcpyHostToDevice));
+      KPM_CUDA(cudaMemcpy(d.cptr, hs.cptr.data(), sizeof(int64_t) * (d.n_chunks + 1), cudaMemcpyHostToDevice));
+      if (hs.sigma > 1) {
+        KPM_CUDA(cudaMemcpy(d.perm, hs.perm.data(), sizeof(int) * d.n_loc, cudaMemcpyHostToDevice));
+        perm_h = hs.perm;
+      }
+      // gather plan of the tiled feed: lcol + fixed-capacity run lists (records per R on use)
+      HostTiles t;
+      build_tiles_host(hs, t);
+      d.tiles_ok = t.ok && t.max_runs <= kMaxRuns;
+      d.max_other = t.max_other;
+      d.max_runs = t.max_runs;
+      if (d.tiles_ok) {
+        std::vector<int> nr(d.n_chunks), rr((size_t)2 * kMaxRuns * d.n_chunks, 0);
+        for (int64_t c = 0; c < d.n_chunks; ++c) {
+          nr[c] = (int)(t.run_ptr[c + 1] - t.run_ptr[c]);
+          for (int64_t k = t.run_ptr[c]; k < t.run_ptr[c + 1]; ++k) {
+            rr[c * 2 * kMaxRuns + 2 * (k - t.run_ptr[c])] = t.runs[2 * k];
+            rr[c * 2 * kMaxRuns + 2 * (k - t.run_ptr[c]) + 1] = t.runs[2 * k + 1];
+          }
+        }
+        if (reserve((void**)&d.lcol, &d.lcol_cap, sizeof(uint16_t) * t.lcol.size()) != cudaSuccess ||
+            reserve((void**)&d.nruns, &d.nruns_cap, sizeof(int) * nr.size()) != cudaSuccess ||
+            reserve((void**)&d.runs, &d.runs_cap, sizeof(int) * rr.size()) != cudaSuccess) {
+          cudaGetLastError();
+          d.tiles_ok = false;  // the other feeds still work
+        } else {
+          KPM_CUDA(cudaMemcpy(d.lcol, t.lcol.data(), sizeof(uint16_t) * t.lcol.size(), cudaMemcpyHostToDevice));
+          KPM_CUDA(cudaMemcpy(d.nruns, nr.data(), sizeof(int) * nr.size(), cudaMemcpyHostToDevice));
+          KPM_CUDA(cudaMemcpy(d.runs, rr.data(), sizeof(int) * rr.size(), cudaMemcpyHostToDevice));
         }
       }
-      if (reserve((void**)&d.lcol, &d.lcol_cap, sizeof(uint16_t) * t.lcol.size()) != cudaSuccess ||
-          reserve((void**)&d.nruns, &d.nruns_cap, sizeof(int) * nr.size()) != cudaSuccess ||
-          reserve((void**)&d.runs, &d.runs_cap, sizeof(int) * rr.size()) != cudaSuccess) {
-        cudaGetLastError();
-        d.tiles_ok = false;  // the other feeds still work
-      } else {
-        KPM_CUDA(cudaMemcpy(d.lcol, t.lcol.data(), sizeof(uint16_t) * t.lcol.size(), cudaMemcpyHostToDevice));
-        KPM_CUDA(cudaMemcpy(d.nruns, nr.data(), sizeof(int) * nr.size(), cudaMemcpyHostToDevice));
-        KPM_CUDA(cudaMemcpy(d.runs, rr.data(), sizeof(int) * rr.size(), cudaMemcpyHostToDevice));
+      halo = hs.halo;
+      ctx->cptr_h = hs.cptr;
+      if (!halo.empty()) {
+        reads_halo.assign(d.n_chunks, 0);
+        for (int64_t c = 0; c < d.n_chunks; ++c)
+          for (int64_t k = hs.cptr[c]; k < hs.cptr[c + 1]; ++k)
+            if (hs.col[k] >= hs.n_pad) {
+              reads_halo[c] = 1;
+              break;
+            }
       }
     }
-    halo = hs.halo;
-    ctx->cptr_h = hs.cptr;
-    if (!halo.empty()) {
-      reads_halo.assign(d.n_chunks, 0);
-      for (int64_t c = 0; c < d.n_chunks; ++c)
-        for (int64_t k = hs.cptr[c]; k < hs.cptr[c + 1]; ++k)
-          if (hs.col[k] >= hs.n_pad) {
-            reads_halo[c] = 1;
-            break;
-          }
+    // a0, last step: row-pair entry order (R18b), on the device for both build paths
+    if (reserve((void**)&d.pinfo, &d.pinfo_cap, sizeof(int) * std::max<int64_t>(1, d.n_chunks)) != cudaSuccess) {
+      cudaGetLastError();
+      reset_sell(ctx->sell);
+      return fail(ctx, KPM_ENOMEM, "device allocation for the pair plan failed");
+    }
+    if (env_int("KPM_PAIR", 1)) {
+      KPM_CUDA(launch_pair_order(d.cptr, d.n_chunks, d.val, d.col, d.tiles_ok ? d.lcol : nullptr, d.pinfo, ctx->stream));
+    } else {
+      KPM_CUDA(cudaMemsetAsync(d.pinfo, 0, sizeof(int) * std::max<int64_t>(1, d.n_chunks), ctx->stream));
+    }
+    KPM_CUDA(cudaStreamSynchronize(ctx->stream));
+    return KPM_OK;
+  };
+  {
+    const kpm_status bst = agree(ctx, build());
+    if (bst != KPM_OK) {
+      if (!ctx->sticky) reset_sell(ctx->sell);
+      return bst;
     }
   }
   if (ctx->opt.nranks == 1 && d.n_halo != 0) return fail(ctx, KPM_EINVAL, "internal: halo on a single rank");
@@ -640,12 +822,18 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
   ctx->fused = false;
   ctx->fused_ready = false;
   ctx->order_h.clear();
+  ctx->order_user = false;
+  ctx->order_id = -3;
+  ctx->auto_order.clear();
+  ctx->adj_state = 0;
+  ctx->adj_ptr.clear();
+  ctx->adj.clear();
   if (ctx->opt.nranks > 1) {
     kpm_status st1 = plan_exchange(ctx, halo, d.n_pad, perm_h, reads_halo);
     if (st1 != KPM_OK) return st1;
-    if ((st1 = apply_order(ctx)) != KPM_OK) return st1;
+    if ((st1 = install_order(ctx, {}, 0)) != KPM_OK) return st1;
     const char* mode = getenv("KPM_HALO");
-    ctx->fused = !(mode && std::string(mode) == "nccl") && ctx->send_runs.size() <= (size_t)kMaxPeerRuns &&
+    ctx->fused = (ctx->vg || !(mode && std::string(mode) == "nccl")) && ctx->send_runs.size() <= (size_t)kMaxPeerRuns &&
                  load_stream_memops();
     if (ctx->fused) {  // Hermitian => symmetric pattern => I receive from exactly the ranks I send to
       std::vector<int> d, r;
@@ -726,6 +914,21 @@ static bool load_stream_memops() {
 // its flag array plus its n_pad; each rank maps the buffers of the peers it sends to and
 // precomputes, per send run, the destination address of the run in the peer's halo slots.
 static kpm_status setup_fused(kpm_ctx* ctx, int Rk) {
+  if (ctx->vg) {  // virtual ranks: the peers' buffers are on this device, plain pointers
+    std::vector<int64_t> all;
+    kpm_status st = allgather_i64(ctx, {(int64_t)ctx->X0, (int64_t)ctx->X1, (int64_t)ctx->flags, ctx->sell.n_pad}, all);
+    if (st != KPM_OK) return st;
+    ctx->dst_x.clear();
+    for (const SendRun& r : ctx->send_runs) {
+      const int64_t off = (all[4 * r.peer + 3] + r.peer_slot) * Rk;
+      ctx->dst_x.push_back({reinterpret_cast<double2*>(all[4 * r.peer]) + off, reinterpret_cast<double2*>(all[4 * r.peer + 1]) + off});
+    }
+    ctx->dst_flag.clear();
+    for (int q : ctx->dest_peers) ctx->dst_flag.push_back(reinterpret_cast<int32_t*>(all[4 * q + 2]) + ctx->opt.rank);
+    ctx->fused_ready = true;
+    ctx->fused_rk = Rk;
+    return KPM_OK;
+  }
   struct Pub {
     cudaIpcMemHandle_t x0, x1, fl;
     int64_t n_pad;
@@ -798,6 +1001,120 @@ static kpm_status plan_tiled_feed(kpm_ctx* ctx, int Rk, bool with_w, int pref_st
   return KPM_OK;
 }
 
+// Block-cache plan (per-position copy records, tile maps, absolute tile rows) of variant v for
+// this grid and chunk order, built once and cached under bc_key.  ok = every tile fits.
+static kpm_status build_bc_plan(kpm_ctx* ctx, int Rk, int v, const TileLayout& tl, int grid, bool& ok) {
+  const DevSell& s = ctx->sell;
+  const bool pair = variant_pair(Rk, v) > 0;
+  const bool wst = variant_wstage(Rk, v);
+  const std::vector<int64_t> key = {Rk, grid, ctx->matrix_gen, ctx->order_gen, tl.stages, wst ? 1 : 0, pair ? 1 : 0,
+                                    tl.pool_slots};
+  if (key == ctx->bc_key) {
+    ok = ctx->bc_ok;
+    return KPM_OK;
+  }
+  ctx->bc_key.clear();
+  const bool mem_ok =
+      reserve((void**)&ctx->bc_rec, &ctx->bc_rec_cap, sizeof(uint4) * kRecSlots * s.n_chunks) == cudaSuccess &&
+      (ctx->opt.nranks == 1 ||
+       reserve((void**)&ctx->bc_rec2, &ctx->bc_rec2_cap, sizeof(uint4) * kRecSlots * s.n_chunks) == cudaSuccess) &&
+      reserve((void**)&ctx->bc_map, &ctx->bc_map_cap, sizeof(int) * kBcMapInts * s.n_chunks) == cudaSuccess &&
+      reserve((void**)&ctx->bc_lcol, &ctx->bc_lcol_cap, sizeof(uint16_t) * s.n_slots) == cudaSuccess &&
+      reserve((void**)&ctx->bc_fail, &ctx->bc_fail_cap, sizeof(int)) == cudaSuccess;
+  if (!mem_ok) {  // no room for the plan: another variant runs
+    cudaGetLastError();
+    ctx->bc_ok = ok = false;
+    ctx->bc_key = key;
+    return KPM_OK;
+  }
+  KPM_CUDA(cudaMemsetAsync(ctx->bc_fail, 0, sizeof(int), ctx->stream));
+  // one plan per launch list (single rank: the chunk order; several ranks: the edge and the
+  // interior list, whose chunks are disjoint, so they share the lcol array)
+  const int* pinfo = pair ? s.pinfo : nullptr;
+  const int relax = 0, ng = 1;
+  if (ctx->opt.nranks == 1) {
+    KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->order_list, s.n_chunks, grid, Rk, wst, tl, ctx->bc_rec,
+                             ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, pinfo, relax, ng, ctx->stream));
+  } else {
+    if (ctx->n_edge)
+      KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->edge_list, ctx->n_edge, grid, Rk, wst, tl,
+                               ctx->bc_rec, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, pinfo, relax, ng, ctx->stream));
+    if (ctx->n_interior)
+      KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->interior_list, ctx->n_interior, grid, Rk, wst, tl,
+                               ctx->bc_rec2, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, pinfo, relax, ng, ctx->stream));
+  }
+  int hfail = 0;
+  KPM_CUDA(cudaMemcpyAsync(&hfail, ctx->bc_fail, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  KPM_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->bc_ok = ok = hfail == 0;
+  ctx->bc_key = key;
+  return KPM_OK;
+}
+
+// The sweep kernel of block width Rk: the requested variant (KPM_VARIANT, else the width's
+// default), or the first later one in table order whose feed fits the matrix (the last entry of
+// every width, the direct feed, always does).  With several ranks every rank takes the same
+// variant: each candidate is agreed on with one allgather, once per matrix (cached).
+static kpm_status select_variant(kpm_ctx* ctx, int Rk, int& variant, TileLayout& tl, int& grid, bool& bc) {
+  const DevSell& s = ctx->sell;
+  const int n = variant_count(Rk);
+  const int lg = __builtin_ctz(Rk);
+  const bool cached = ctx->chosen_gen[lg] == ctx->matrix_gen && ctx->chosen_ovr[lg] == ctx->variant_override;
+  std::vector<int> cand;
+  if (cached) {
+    cand.push_back(ctx->chosen[lg]);
+  } else {
+    if (ctx->variant_override >= 0 && ctx->variant_override < n) cand.push_back(ctx->variant_override);
+    for (int v = 0; v < n; ++v)
+      if (cand.empty() || v != cand[0]) cand.push_back(v);
+  }
+  for (int v : cand) {
+    TileLayout pl;
+    bool ok = true;
+    const int bcc = variant_bc(Rk, v);
+    kpm_status st;
+    if (bcc) {
+      pl = s.tiles_ok ? plan_tiles_bc(Rk, s.max_width, variant_wstage(Rk, v), variant_stages(Rk, v), bcc)
+                      : TileLayout();
+      ok = pl.stages >= 1;
+    } else if (variant_tiled(Rk, v)) {
+      if ((st = plan_tiled_feed(ctx, Rk, variant_wstage(Rk, v), variant_stages(Rk, v), pl)) != KPM_OK) return st;
+      ok = pl.stages >= 1;
+    } else if (variant_staged(Rk, v)) {
+      ok = s.max_width <= staged_max_width();
+    }
+    int g = 1;
+    if (ok) {
+      const int dyn = variant_tiled(Rk, v) ? pl.pool_bytes + pl.stages * pl.stage_bytes : 0;
+      const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, sweep_occupancy(Rk, v, dyn));
+      g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * occ, s.n_chunks));
+      if ((st = ensure_order(ctx, g, bcc > 0, Rk)) != KPM_OK) return st;
+      if (bcc && (st = build_bc_plan(ctx, Rk, v, pl, g, ok)) != KPM_OK) return st;
+    }
+    if (ctx->opt.nranks > 1 && !cached) {  // agree, so that every rank runs the same launches
+      std::vector<int64_t> all;
+      if ((st = allgather_i64(ctx, {ok ? 1 : 0}, all)) != KPM_OK) return st;
+      for (int64_t x : all) ok = ok && x == 1;
+    }
+    if (ok) {
+      // re-install the chosen kernel's order (a plan tried after it may have replaced it; both
+      // calls are no-ops when nothing changed)
+      if ((st = ensure_order(ctx, g, bcc > 0, Rk)) != KPM_OK) return st;
+      if (bcc && (st = build_bc_plan(ctx, Rk, v, pl, g, ok)) != KPM_OK) return st;
+      if (!ok) return fail(ctx, KPM_ESTATE, "internal: block-cache plan changed");
+      variant = v;
+      tl = pl;
+      grid = g;
+      bc = bcc > 0;
+      ctx->chosen[lg] = v;
+      ctx->chosen_gen[lg] = ctx->matrix_gen;
+      ctx->chosen_ovr[lg] = ctx->variant_override;
+      return KPM_OK;
+    }
+  }
+  return fail(ctx, KPM_ESTATE, cached ? "internal: the cached kernel variant no longer fits" : "no kernel variant fits");
+}
+
 static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint64_t seed, const double* v0,
                             double2* eta_cols, bool first, bool last) {
   const int Rk = block_width(rb);
@@ -806,11 +1123,14 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   const int64_t n_rows_total = s.n_pad + s.n_halo;
   kpm_status st;
   size_t xcap = ctx->x_cap;
-  if ((st = ensure(ctx, (void**)&ctx->X0, &xcap, (size_t)n_rows_total * Rk, sizeof(double2))) != KPM_OK) return st;
-  xcap = ctx->x_cap;
-  if ((st = ensure(ctx, (void**)&ctx->X1, &xcap, (size_t)n_rows_total * Rk, sizeof(double2))) != KPM_OK) return st;
-  if (xcap != ctx->x_cap) ctx->fused_ready = false;
-  ctx->x_cap = xcap;
+  st = ensure(ctx, (void**)&ctx->X0, &xcap, (size_t)n_rows_total * Rk, sizeof(double2));
+  if (st == KPM_OK) {
+    xcap = ctx->x_cap;
+    st = ensure(ctx, (void**)&ctx->X1, &xcap, (size_t)n_rows_total * Rk, sizeof(double2));
+    if (xcap != ctx->x_cap) ctx->fused_ready = false;
+    if (st == KPM_OK) ctx->x_cap = xcap;
+  }
+  if ((st = agree(ctx, st)) != KPM_OK) return st;
   if (ctx->opt.nranks > 1 && ctx->fused) {  // collective: re-publish when any rank's buffers changed
     std::vector<int64_t> all;
     if ((st = allgather_i64(ctx, {ctx->fused_ready && ctx->fused_rk == Rk ? 1 : 0}, all)) != KPM_OK) return st;
@@ -834,115 +1154,42 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     }
   }
 
-  const int lg = __builtin_ctz(Rk);
-  auto tiled_plan = [&](bool with_w, int pref_stages, TileLayout& plan) {
-    return plan_tiled_feed(ctx, Rk, with_w, pref_stages, plan);
-  };
-  auto usable = [&](int v) {
-    if (variant_bc(Rk, v))  // block cache: fits the layout
-      return s.tiles_ok &&
-             plan_tiles_bc(Rk, s.max_width, variant_wstage(Rk, v), variant_stages(Rk, v), variant_bc(Rk, v)).stages >= 1;
-    if (variant_tiled(Rk, v)) {
-      TileLayout pl;
-      return tiled_plan(variant_wstage(Rk, v), variant_stages(Rk, v), pl) == KPM_OK && pl.stages >= 1;
-    }
-    if (variant_staged(Rk, v)) return s.max_width <= staged_max_width();
-    return true;
-  };
-  int variant = 0;
-  if (ctx->variant_override >= 0 && ctx->variant_override < variant_count(Rk)) variant = ctx->variant_override;
-  if (!usable(variant))
-    for (variant = 0; variant < variant_count(Rk) - 1 && !usable(variant); ++variant) {
-    }
-  TileLayout plan;
-  const bool bc = variant_bc(Rk, variant) > 0;
-  if (bc)
-    plan = plan_tiles_bc(Rk, s.max_width, variant_wstage(Rk, variant), variant_stages(Rk, variant),
-                         variant_bc(Rk, variant));
-  else if (variant_tiled(Rk, variant) &&
-           (st = tiled_plan(variant_wstage(Rk, variant), variant_stages(Rk, variant), plan)) != KPM_OK)
-    return st;
-  const int rec_index = 2 * lg + (variant_wstage(Rk, variant) ? 1 : 0);
+  int variant = 0, grid = 1;
+  TileLayout tl;
+  bool bc = false;
+  if ((st = select_variant(ctx, Rk, variant, tl, grid, bc)) != KPM_OK) return st;
+  const int rec_index = 2 * __builtin_ctz(Rk) + (variant_wstage(Rk, variant) ? 1 : 0);
   ctx->last_variant = variant_name(Rk, variant);
-  const TileLayout tl = plan;
-  const int dyn_smem = variant_tiled(Rk, variant) ? tl.pool_bytes + tl.stages * tl.stage_bytes : 0;
-  const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, sweep_occupancy(Rk, variant, dyn_smem));
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * occ, s.n_chunks));
-  if (bc) {  // per-position records for this grid and chunk order (built once, cached)
-    const std::vector<int64_t> key = {Rk, grid, ctx->matrix_gen, tl.stages, variant_wstage(Rk, variant) ? 1 : 0};
-    if (key != ctx->bc_key) {
-      ctx->bc_key.clear();
-      const bool mem_ok =
-          reserve((void**)&ctx->bc_rec, &ctx->bc_rec_cap, sizeof(uint4) * kRecSlots * s.n_chunks) == cudaSuccess &&
-          (ctx->opt.nranks == 1 ||
-           reserve((void**)&ctx->bc_rec2, &ctx->bc_rec2_cap, sizeof(uint4) * kRecSlots * s.n_chunks) == cudaSuccess) &&
-          reserve((void**)&ctx->bc_map, &ctx->bc_map_cap, sizeof(int) * kBcMapInts * s.n_chunks) == cudaSuccess &&
-          reserve((void**)&ctx->bc_lcol, &ctx->bc_lcol_cap, sizeof(uint16_t) * s.n_slots) == cudaSuccess &&
-          reserve((void**)&ctx->bc_fail, &ctx->bc_fail_cap, sizeof(int)) == cudaSuccess;
-      if (!mem_ok) {  // no room for the plan: the base variant runs (below)
-        cudaGetLastError();
-        ctx->bc_ok = false;
-        ctx->bc_key = key;
-      }
-    }
-    if (key != ctx->bc_key) {
-      KPM_CUDA(cudaMemsetAsync(ctx->bc_fail, 0, sizeof(int), ctx->stream));
-      // one plan per launch list (single rank: the chunk order; several ranks: the edge and the
-      // interior list, whose chunks are disjoint, so they share the lcol array)
-      const bool wst = variant_wstage(Rk, variant);
-      if (ctx->opt.nranks == 1) {
-        KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->order_list, s.n_chunks, grid, Rk, wst, tl,
-                                 ctx->bc_rec, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, ctx->stream));
-      } else {
-        if (ctx->n_edge)
-          KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->edge_list, ctx->n_edge, grid, Rk, wst, tl,
-                                   ctx->bc_rec, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, ctx->stream));
-        if (ctx->n_interior)
-          KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->interior_list, ctx->n_interior, grid, Rk, wst,
-                                   tl, ctx->bc_rec2, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, ctx->stream));
-      }
-      int hfail = 0;
-      KPM_CUDA(cudaMemcpyAsync(&hfail, ctx->bc_fail, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-      KPM_CUDA(cudaStreamSynchronize(ctx->stream));
-      ctx->bc_ok = hfail == 0;
-      ctx->bc_key = key;
-    }
-    if (!ctx->bc_ok) {  // some tile does not fit the pool: rerun with the width's base variant
-      const int saved = ctx->variant_override;
-      ctx->variant_override = base_variant(Rk);
-      const kpm_status r = run_block(ctx, M, rb, col_begin, seed, v0, eta_cols, first, last);
-      ctx->variant_override = saved;
-      return r;
-    }
-  }
   const bool multi = ctx->opt.nranks > 1;
   const int parts = multi ? 2 : 1;  // edge + interior launches per sweep
   const size_t per_sweep = (size_t)3 * Rk * grid * parts;
-  if ((st = ensure(ctx, (void**)&ctx->partials, &ctx->partials_cap, per_sweep * n_sweeps, sizeof(double))) != KPM_OK)
-    return st;
+  st = ensure(ctx, (void**)&ctx->partials, &ctx->partials_cap, per_sweep * n_sweeps, sizeof(double));
   size_t ecap = ctx->eta_cap;
-  if ((st = ensure(ctx, (void**)&ctx->eta_even, &ecap, (size_t)n_sweeps * kMaxBlockWidth, sizeof(double2))) != KPM_OK)
-    return st;
-  ecap = ctx->eta_cap;
-  if ((st = ensure(ctx, (void**)&ctx->eta_odd, &ecap, (size_t)n_sweeps * kMaxBlockWidth, sizeof(double2))) != KPM_OK)
-    return st;
-  if (ecap > ctx->eta_cap || !ctx->h_eta) {
+  if (st == KPM_OK) st = ensure(ctx, (void**)&ctx->eta_even, &ecap, (size_t)n_sweeps * kMaxBlockWidth, sizeof(double2));
+  if (st == KPM_OK) {
+    ecap = ctx->eta_cap;
+    st = ensure(ctx, (void**)&ctx->eta_odd, &ecap, (size_t)n_sweeps * kMaxBlockWidth, sizeof(double2));
+  }
+  if (st == KPM_OK && (ecap > ctx->eta_cap || !ctx->h_eta)) {
     if (ctx->h_eta) cudaFreeHost(ctx->h_eta);
     ctx->h_eta = nullptr;
     if (cudaMallocHost((void**)&ctx->h_eta, sizeof(double2) * 2 * ecap) != cudaSuccess) {
       cudaGetLastError();
-      return fail(ctx, KPM_ENOMEM, "pinned host allocation failed");
+      st = fail(ctx, KPM_ENOMEM, "pinned host allocation failed");
     }
   }
-  ctx->eta_cap = ecap;
+  if (st == KPM_OK) ctx->eta_cap = ecap;
+  if (v0 && st == KPM_OK) {
+    size_t vcap = ctx->v0_cap;
+    st = ensure(ctx, (void**)&ctx->v0_dev, &vcap, (size_t)s.n_loc * rb, sizeof(double2));
+    if (st == KPM_OK) ctx->v0_cap = vcap;
+  }
+  if ((st = agree(ctx, st)) != KPM_OK) return st;
 
   cudaStream_t str = ctx->stream;
   if (first) KPM_CUDA(cudaEventRecord(ctx->ev[0], str));
   // a1: start block
   if (v0) {
-    size_t vcap = ctx->v0_cap;
-    if ((st = ensure(ctx, (void**)&ctx->v0_dev, &vcap, (size_t)s.n_loc * rb, sizeof(double2))) != KPM_OK) return st;
-    ctx->v0_cap = vcap;
     KPM_CUDA(cudaMemcpyAsync(ctx->v0_dev, v0, sizeof(double2) * s.n_loc * rb, cudaMemcpyHostToDevice, str));
     KPM_CUDA(launch_v0_upload_permute(ctx->X0, ctx->X1, ctx->v0_dev, s.perm, s.n_loc, s.n_pad, n_rows_total, Rk, rb, str));
     if (multi && (st = exchange_halo(ctx, ctx->X0, Rk, str)) != KPM_OK) return st;
@@ -1026,8 +1273,19 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     KPM_CUDA(launch_aug_spmmv(Rk, variant, init, sa, grid, str));
     return KPM_OK;
   };
+  // KPM_TIMING: an event before the init sweep and after every sweep (no graph, per-launch)
+  const bool timing = (ctx->opt.flags & KPM_TIMING) != 0;
+  if (timing) {
+    while ((int)ctx->sweep_ev.size() < n_sweeps + 1) {
+      cudaEvent_t e;
+      KPM_CUDA(cudaEventCreate(&e));
+      ctx->sweep_ev.push_back(e);
+    }
+    KPM_CUDA(cudaEventRecord(ctx->sweep_ev[0], str));
+  }
   // a2: init sweep, eta_0, eta_1
   if ((st = sweep(0)) != KPM_OK) return st;
+  if (timing) KPM_CUDA(cudaEventRecord(ctx->sweep_ev[1], str));
   // a3: main sweeps, eta_2m, eta_2m+1.  Single rank: the M/2-1 launches are captured once
   // into a CUDA graph per configuration and replayed (launch overhead matters for small
   // matrices, e.g. C1's 5-us sweeps); env KPM_GRAPH=0 launches them one by one.
@@ -1035,12 +1293,14 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   // graphs pay off only when a sweep is short (launch overhead ~ 4 us vs the sweep); for large
   // matrices a re-capture after every kpm_set_matrix would cost more than it saves
   const double sweep_bytes = 20.0 * (double)s.n_slots + 48.0 * Rk * (double)s.n_pad;
-  const bool use_graph = !multi && ctx->use_graph && n_sweeps > 2 && sweep_bytes < 512e6;
+  const bool use_graph = !multi && !timing && ctx->use_graph && n_sweeps > 2 && sweep_bytes < 512e6;
   if (use_graph) {
+    int64_t abits, bbits;  // the exact scale factors (bit patterns) the captured launches carry
+    std::memcpy(&abits, &ctx->a, sizeof abits);
+    std::memcpy(&bbits, &ctx->b, sizeof bbits);
     const std::vector<int64_t> key = {Rk, variant, grid, n_sweeps, (int64_t)ctx->X0, (int64_t)ctx->X1,
                                       (int64_t)ctx->partials, (int64_t)sa.chunk_list, (int64_t)sa.rec,
-                                      (int64_t)s.val, (int64_t)(ctx->a * 1e15), (int64_t)(ctx->b * 1e15),
-                                      ctx->matrix_gen, tl.stages};
+                                      (int64_t)s.val, abits, bbits, ctx->matrix_gen, ctx->order_gen, tl.stages};
     if (!ctx->graph_exec || key != ctx->graph_key) {
       if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
       ctx->graph_exec = nullptr;
@@ -1048,7 +1308,8 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
       KPM_CUDA(cudaStreamBeginCapture(str, cudaStreamCaptureModeThreadLocal));
       for (int m = 1; m < n_sweeps; ++m)
         if ((st = sweep(m)) != KPM_OK) {
-          cudaStreamEndCapture(str, &g);
+          if (cudaStreamEndCapture(str, &g) == cudaSuccess && g) cudaGraphDestroy(g);
+          cudaGetLastError();
           return st;
         }
       KPM_CUDA(cudaStreamEndCapture(str, &g));
@@ -1058,13 +1319,32 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     }
     KPM_CUDA(cudaGraphLaunch(ctx->graph_exec, str));
   } else {
-    for (int m = 1; m < n_sweeps; ++m)
+    for (int m = 1; m < n_sweeps; ++m) {
       if ((st = sweep(m)) != KPM_OK) return st;
+      if (timing) KPM_CUDA(cudaEventRecord(ctx->sweep_ev[m + 1], str));
+    }
   }
   KPM_CUDA(cudaEventRecord(ctx->ev[2], str));
   // a4: deterministic grid reduction of all sweeps' partials
   KPM_CUDA(launch_eta_finalize(ctx->partials, n_sweeps, Rk, grid * parts, ctx->eta_even, ctx->eta_odd, str));
-  if (multi) {  // a6: the single global reduction, once, at the end (Table III)
+  if (multi && ctx->vg) {  // virtual ranks: host all-gather, sum in rank order, back to the device
+    const size_t ne = (size_t)n_sweeps * Rk * 2;
+    std::vector<int64_t> mine(2 * ne);
+    KPM_CUDA(cudaMemcpyAsync(mine.data(), ctx->eta_even, sizeof(double) * ne, cudaMemcpyDeviceToHost, str));
+    KPM_CUDA(cudaMemcpyAsync(mine.data() + ne, ctx->eta_odd, sizeof(double) * ne, cudaMemcpyDeviceToHost, str));
+    KPM_CUDA(cudaStreamSynchronize(str));
+    const auto all = ctx->vg->allgatherv(ctx->opt.rank, mine);
+    std::vector<double> sum(2 * ne, 0.0);
+    for (const auto& v : all)
+      for (size_t i = 0; i < 2 * ne; ++i) {
+        double x;
+        std::memcpy(&x, &v[i], sizeof x);
+        sum[i] += x;
+      }
+    KPM_CUDA(cudaMemcpyAsync(ctx->eta_even, sum.data(), sizeof(double) * ne, cudaMemcpyHostToDevice, str));
+    KPM_CUDA(cudaMemcpyAsync(ctx->eta_odd, sum.data() + ne, sizeof(double) * ne, cudaMemcpyHostToDevice, str));
+    KPM_CUDA(cudaStreamSynchronize(str));
+  } else if (multi) {  // a6: the single global reduction, once, at the end (Table III)
     KPM_NCCL(ncclAllReduce(ctx->eta_even, ctx->eta_even, (size_t)n_sweeps * Rk * 2, ncclDouble, ncclSum, ctx->comm, str));
     KPM_NCCL(ncclAllReduce(ctx->eta_odd, ctx->eta_odd, (size_t)n_sweeps * Rk * 2, ncclDouble, ncclSum, ctx->comm, str));
   }
@@ -1087,6 +1367,11 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     ctx->last_sweep_ms = 0.0;
     ctx->last_n_sweeps = 0;
   }
+  if (timing)
+    for (int m = 0; m < n_sweeps; ++m) {
+      KPM_CUDA(cudaEventElapsedTime(&ms, ctx->sweep_ev[m], ctx->sweep_ev[m + 1]));
+      ctx->sweep_times.push_back(ms);
+    }
   if (last) {
     KPM_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]));
     ctx->last_total_ms = ms;
@@ -1130,6 +1415,7 @@ static kpm_status moments_common(kpm_ctx* ctx, int M, int R, uint64_t seed, cons
   if (R < 1) return fail(ctx, KPM_EINVAL, "R must be >= 1");
   if (!mu) return fail(ctx, KPM_EINVAL, "mu is NULL");
   KPM_CUDA(cudaSetDevice(ctx->opt.device));
+  ctx->sweep_times.clear();
   std::vector<double2> eta_all((size_t)R * M);
   const int64_t n_loc = ctx->sell.n_loc;
   std::vector<double> v0_block;
@@ -1368,5 +1654,52 @@ extern "C" kpm_status kpm_export_sell(const kpm_ctx* ctx_c, double* val, int32_t
   if (perm && !s.perm)
     for (int64_t p = 0; p < s.n_loc; ++p) perm[p] = (int32_t)p;  // sigma = 1: identity
   if (halo && !ctx->halo.empty()) std::memcpy(halo, ctx->halo.data(), sizeof(int64_t) * ctx->halo.size());
+  return KPM_OK;
+}
+
+extern "C" kpm_status kpm_export_pairs(const kpm_ctx* ctx_c, int32_t* pinfo) {
+  kpm_ctx* ctx = const_cast<kpm_ctx*>(ctx_c);
+  if (!ctx || !pinfo) return KPM_EINVAL;
+  if (!ctx->have_matrix) return fail(ctx, KPM_ESTATE, "no matrix");
+  KPM_CUDA(cudaSetDevice(ctx->opt.device));
+  KPM_CUDA(cudaMemcpy(pinfo, ctx->sell.pinfo, sizeof(int32_t) * ctx->sell.n_chunks, cudaMemcpyDeviceToHost));
+  return KPM_OK;
+}
+
+extern "C" kpm_status kpm_last_sweep_times(const kpm_ctx* ctx, double* ms, int64_t* n) {
+  if (!ctx || !n) return KPM_EINVAL;
+  const int64_t have = (int64_t)ctx->sweep_times.size();
+  if (ms) {
+    const int64_t k = std::min(*n, have);
+    std::memcpy(ms, ctx->sweep_times.data(), sizeof(double) * k);
+    *n = k;
+  } else {
+    *n = have;
+  }
+  return KPM_OK;
+}
+
+extern "C" kpm_status kpm_export_halo(const kpm_ctx* ctx_c, int64_t* n_recv, int64_t* recv, int64_t* n_send,
+                                      int64_t* send) {
+  kpm_ctx* ctx = const_cast<kpm_ctx*>(ctx_c);
+  if (!ctx || !n_recv || !n_send) return KPM_EINVAL;
+  if (!ctx->have_matrix) return fail(ctx, KPM_ESTATE, "no matrix");
+  const int64_t nr = (int64_t)ctx->recv_runs.size(), ns = (int64_t)ctx->send_runs.size();
+  if (recv) {
+    if (*n_recv < nr) return fail(ctx, KPM_EINVAL, "recv capacity too small");
+    for (int64_t i = 0; i < nr; ++i) {
+      const RecvRun& r = ctx->recv_runs[i];
+      recv[4 * i] = r.peer, recv[4 * i + 1] = r.gfirst, recv[4 * i + 2] = r.count, recv[4 * i + 3] = r.slot;
+    }
+  }
+  if (send) {
+    if (*n_send < ns) return fail(ctx, KPM_EINVAL, "send capacity too small");
+    for (int64_t i = 0; i < ns; ++i) {
+      const SendRun& r = ctx->send_runs[i];
+      send[4 * i] = r.peer, send[4 * i + 1] = r.pos, send[4 * i + 2] = r.count, send[4 * i + 3] = r.peer_slot;
+    }
+  }
+  *n_recv = nr;
+  *n_send = ns;
   return KPM_OK;
 }

@@ -1,10 +1,12 @@
-// Host-only diagnostic exports of the halo-exchange planning (include/kpm.h, kpm_plan_*).
+// Host-only diagnostic exports of the halo-exchange planning and the chunk order (include/kpm.h,
+// kpm_plan_*).
 // They run the same functions kpm_set_matrix uses (halo_plan.cpp) without CUDA or NCCL, so
 // the multi-rank index logic is testable on a CPU (tests/test_halo_plan.py).
 #include <algorithm>
 #include <vector>
 
 #include "../../include/kpm.h"
+#include "chunk_order.h"
 #include "halo_plan.h"
 
 using namespace kpm;
@@ -53,5 +55,20 @@ extern "C" kpm_status kpm_plan_send(int64_t row_begin, int64_t row_end, int peer
     }
   }
   *n_runs = (int64_t)out.size();
+  return KPM_OK;
+}
+
+extern "C" kpm_status kpm_plan_chunk_order(int64_t n_chunks, const int64_t* nbr_ptr, const int64_t* nbr, int64_t grid,
+                                           const int8_t* skip, int64_t* order) {
+  if (n_chunks < 0 || !nbr_ptr || (nbr_ptr[n_chunks] > 0 && !nbr) || grid < 1 || !order) return KPM_EINVAL;
+  std::vector<int64_t> ptr(nbr_ptr, nbr_ptr + n_chunks + 1), nb(nbr, nbr + nbr_ptr[n_chunks]);
+  for (int64_t c = 0; c < n_chunks; ++c)
+    if (ptr[c + 1] < ptr[c]) return KPM_EINVAL;
+  for (int64_t b : nb)
+    if (b < 0 || b >= n_chunks) return KPM_ERANGE;
+  std::vector<char> sk;
+  if (skip) sk.assign(skip, skip + n_chunks);
+  const std::vector<int64_t> o = line_order(n_chunks, ptr, nb, grid, sk);
+  std::copy(o.begin(), o.end(), order);
   return KPM_OK;
 }

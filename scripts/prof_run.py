@@ -18,11 +18,16 @@ def main():
     ap.add_argument("--M", type=int, default=8)
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--sigma", type=int, default=1)
+    ap.add_argument("--variant", default="", help="kernel variant name (KPM_VARIANT by name)")
     ap.add_argument("--order", default="ylines", choices=["ylines", "storage"],
                     help="ylines: the bench's chunk order at R = 16 / 32 (block-cache feed)")
     args = ap.parse_args()
     import paper_1410_5242_b200 as kpm
 
+    if args.variant:
+        R0 = int(args.R.split(",")[0])
+        names = [kpm.variant_name(R0, v) for v in range(32)]
+        os.environ["KPM_VARIANT"] = str(names.index(args.variant))
     nx, ny, nz = (int(t) for t in args.lattice.split(","))
     lat = Lattice(nx, ny, nz)
     rp, col, val = generate_csr(lat)
@@ -36,11 +41,14 @@ def main():
                 from workloads.ti_lattice import chunk_order_ylines
                 sms = torch.cuda.get_device_properties(0).multi_processor_count
                 ctas = {16: 2, 32: 1}.get(R)  # default block-cache feed CTAs per SM (kernels.cu)
+                if args.variant.startswith("pair"):
+                    ctas = 1
                 ctx.set_chunk_order(chunk_order_ylines(lat, sms * ctas) if ctas else None)
             for _ in range(args.reps):
                 mu, _ = ctx.moments(args.M, R, SEED, want_eta=False)
             t, s, n = ctx.last_timing()
-            print(f"R={R} M={args.M} total_ms={t:.3f} sweep_ms={s:.4f} mu0={mu[0]:.0f}", flush=True)
+            print(f"R={R} M={args.M} total_ms={t:.3f} sweep_ms={s:.4f} mu0={mu[0]:.0f} kernel={ctx.last_kernel()}",
+                  flush=True)
 
 
 if __name__ == "__main__":

@@ -35,6 +35,12 @@ def problem(dims, potential=None, periodic_z=False):
     return lat, rp, col, val, a, b
 
 
+def ref_sell(rp, col, val, **kw):
+    """The product's SELL contract: the R18 layout of sell_ref.build_sell, then the row-pair
+    entry order (sell_ref.pair_order, R18b)."""
+    return sell_ref.pair_order(sell_ref.build_sell(rp, col, val, **kw))
+
+
 def check(eta_g, mu_g, eta_o, cols=None):
     if cols is not None:
         eta_g = eta_g[cols]
@@ -80,9 +86,11 @@ def test_zero_potential_and_sigma(pkg, sigma):
         ctx.set_matrix(rp, col, val, a, b)
         mu, eta = ctx.moments(M, R, 77)
         s = ctx.export_sell()
+        s["pinfo"] = ctx.export_pairs()
     eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, 77)
     check(eta, mu, eta_o)
-    ref = sell_ref.build_sell(rp, col, val, C=32, sigma=sigma)
+    ref = ref_sell(rp, col, val, C=32, sigma=sigma)
+    assert np.array_equal(s["pinfo"], ref["pinfo"])
     assert np.array_equal(s["cptr"], ref["cptr"])
     assert np.array_equal(s["col"], ref["col"])
     assert np.array_equal(s["val"], ref["val"])
@@ -94,10 +102,12 @@ def test_sell_bit_exact_c1(pkg):
     with pkg.KpmContext() as ctx:
         ctx.set_matrix(rp, col, val, a, b)
         s = ctx.export_sell()
-    ref = sell_ref.build_sell(rp, col, val)
-    for k in ("cptr", "col", "val", "perm"):
+        s["pinfo"] = ctx.export_pairs()
+    ref = ref_sell(rp, col, val)
+    for k in ("cptr", "col", "val", "perm", "pinfo"):
         assert np.array_equal(s[k], ref[k]), k
     assert s["cptr"][-1] == 13 * lat.n
+    assert np.all(s["pinfo"] == (3 | 8 << 8))  # TI: orbitals {0,3}, {1,2} share 8 columns
 
 
 def test_exact_trace_bloch_v0(pkg):
@@ -265,10 +275,11 @@ def test_device_build(pkg, dims):
         with pkg.KpmContext() as ctx:
             ctx.set_matrix(rp_d, col_d, val_d, a, b, n_global=lat.n, mem=pkg.KPM_MEM_DEVICE)
             s = ctx.export_sell()
+            s["pinfo"] = ctx.export_pairs()
             mu, eta = ctx.moments(M, R, SEED)
-            assert ctx.last_kernel().startswith("tiled")
-        ref = sell_ref.build_sell(rp, col, val)
-        for k in ("cptr", "col", "val", "perm"):
+            assert ctx.last_kernel().startswith(("tiled", "pair"))
+        ref = ref_sell(rp, col, val)
+        for k in ("cptr", "col", "val", "perm", "pinfo"):
             assert np.array_equal(s[k], ref[k]), k
         check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, M, R, SEED))
     torch.cuda.synchronize()
@@ -322,7 +333,7 @@ def test_rows_without_diagonal(pkg, R):
 
     M = 64
     eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, SEED)
-    ref = sell_ref.build_sell(rp, col, val)
+    ref = ref_sell(rp, col, val)
     for dev in (False, True):  # host builder, device builder
         with pkg.KpmContext() as ctx:
             if dev:
@@ -331,7 +342,7 @@ def test_rows_without_diagonal(pkg, R):
             else:
                 ctx.set_matrix(rp, col, val, a, b)
             mu, eta = ctx.moments(M, R, SEED)
-            assert ctx.last_kernel().startswith("tiled")
+            assert ctx.last_kernel().startswith(("tiled", "pair"))
             s = ctx.export_sell()
         check(eta, mu, eta_o)
         assert np.array_equal(s["col"], ref["col"]) and np.array_equal(s["val"], ref["val"])
@@ -416,7 +427,7 @@ def test_host_builder_forced(pkg, sigma, monkeypatch):
         ctx.set_matrix(rp, col, val, a, b)
         s = ctx.export_sell()
         mu, eta = ctx.moments(40, 8, SEED)
-    ref = sell_ref.build_sell(rp, col, val, C=32, sigma=sigma)
+    ref = ref_sell(rp, col, val, C=32, sigma=sigma)
     for k in ("cptr", "col", "val", "perm"):
         assert np.array_equal(s[k], ref[k]), k
     check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, 40, 8, SEED))
@@ -522,3 +533,77 @@ def test_check_hermitian_flag(pkg):
         assert e.value.status == pkg.KPM_EINVAL
     with pkg.KpmContext() as ctx:
         ctx.set_matrix(rp2, col2, val2, a, b)  # unchecked by default
+
+
+def test_bench_config_c3_full_m(pkg):
+    """The headline configuration exactly as bench.py times it: C3 200x100x40, M = 2000, R = 32,
+    the width's default kernel and the library's default chunk order.  Columns 0, 7, 19, 31
+    element by element against the oracle (1e-10 per column, R10; ~2 min of oracle
+    time), bitwise run-to-run reproducible, mu_0 = N."""
+    lat, rp, col, val, a, b = problem((200, 100, 40))
+    M, R = 2000, 32
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments(M, R, SEED)
+        assert ctx.last_kernel() == pkg.variant_name(R, 0)
+        mu2, eta2 = ctx.moments(M, R, SEED)
+    assert np.array_equal(eta, eta2) and np.array_equal(mu, mu2)
+    assert mu[0] == lat.n and np.all(np.abs(mu) <= mu[0])
+    threads = oracle.max_threads()
+    for c in (0, 7, 19, 31):
+        eta_o = oracle.kpm_eta(rp, col, val, a, b, M, 1, SEED, col_begin=c, threads=threads)
+        check(eta[c : c + 1], None, eta_o, cols=[0])
+
+
+@pytest.mark.parametrize("R", [1, 32])
+def test_z4_start_block_bit_exact(pkg, R):
+    """|rand()>: the device Z4 block equals the oracle's independent Philox copy bit for
+    bit -- read back through the plain SpMMV W = H V with H = 1 (exact), on a ragged row count."""
+    n = 1000
+    rp = np.arange(n + 1, dtype=np.int64)
+    col = np.arange(n, dtype=np.int64)
+    val = np.ones(n, dtype=np.complex128)
+    seed = 0x5EED + R
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, 1.0, 0.0)
+        _, w = ctx.sweep_kernel("spmmv", R, seed, n_sweeps=1, want_w=True)
+    assert np.array_equal(w, oracle.z4_block(0, n, 0, R, seed))
+
+
+def test_z4_later_column_blocks_exact_arithmetic(pkg):
+    """Columns 32..63 (the second block of 32, col_begin = 32) and the per-column stage (col_begin
+    = r): on a ring with hopping 1, a = 1/4, b = 0 every eta is a dyadic rational computed exactly,
+    so GPU and oracle agree bit for bit iff their start vectors do."""
+    n = 4000
+    i = np.arange(n)
+    rows = np.concatenate([i, i])
+    cols = np.concatenate([(i + 1) % n, (i - 1) % n])
+    order = np.lexsort((cols, rows))
+    col = cols[order].astype(np.int64)
+    rp = np.arange(0, 2 * n + 1, 2, dtype=np.int64)
+    val = np.ones(2 * n, dtype=np.complex128)
+    M, R, seed = 8, 64, 99
+    eta_o = oracle.kpm_eta(rp, col, val, 0.25, 0.0, M, R, seed)
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, 0.25, 0.0)
+        _, eta = ctx.moments(M, R, seed)
+        _, eta1 = ctx.moments_stage("aug_spmv", M, 4, seed)
+    assert np.array_equal(eta, eta_o)
+    assert np.array_equal(eta1, eta_o[:4])
+
+
+def test_per_sweep_timing(pkg):
+    """KPM_TIMING: one device time per sweep (init + M/2 - 1 main sweeps), consistent with the
+    call's total; without the flag no per-sweep times."""
+    lat, rp, col, val, a, b = problem((8, 8, 8))
+    with pkg.KpmContext(flags=pkg.KPM_TIMING | pkg.KPM_DETERMINISTIC) as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        ctx.moments(64, 4, SEED)
+        t = ctx.sweep_times()
+        total, sweep, n = ctx.last_timing()
+    assert len(t) == 32 and np.all(t > 0) and t.sum() <= total * 1.001
+    assert abs(np.mean(t[1:]) - sweep) <= 0.05 * sweep + 1e-3
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        ctx.moments(64, 4, SEED)
+        assert len(ctx.sweep_times()) == 0
