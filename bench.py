@@ -31,7 +31,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from workloads.ti_lattice import (CONFIGS, SEED, Lattice, chunk_order_yband, chunk_order_ylines, gershgorin, generate_csr,  # noqa: E402
+from workloads.ti_lattice import (CONFIGS, SEED, Lattice, chunk_order_ylines, gershgorin, generate_csr,  # noqa: E402
                                   generate_csr_torch, scale_factors)
 
 S_D, S_I = 16, 4
@@ -106,21 +106,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-def cache_roofline(wavefronts, sm_mhz, sweep_ms, t_hbm_ms):
-    """The paper's custom roofline P* = min(P*_MEM, P*_LLC) (Eq. (11) `eq:roofline_custom`)
-    for the B200: the shared-memory data pipe moves one 128-B wavefront per cycle per SM, so a
-    sweep needs at least W / (148 f_SM) seconds for the W wavefronts ncu counted per launch
-    (profiles/traffic.json), at the SM clock sampled during the timed region."""
-    if not wavefronts or not sm_mhz:
-        return None
-    t_smem = wavefronts / (148 * sm_mhz * 1e6) * 1e3
-    t_bound = max(t_smem, t_hbm_ms)
-    return {"bound": "smem" if t_smem > t_hbm_ms else "hbm", "smem_wavefronts_per_launch": wavefronts,
-            "sm_mhz": sm_mhz, "t_smem_min_ms": t_smem, "t_hbm_min_ms": t_hbm_ms, "t_measured_ms": sweep_ms,
-            "frac_of_applicable": t_bound / sweep_ms,
-            "note": "wavefronts from ncu --set full (profiles/), peak 1 wavefront/clk/SM x 148 SMs"}
-
-
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -135,21 +120,24 @@ def build_problem(nx, ny, nz):
     return lat, rp, col, val, a, b
 
 
-def oracle_sample(rp, col, val, a, b, n, nnz, target_s=15.0, max_sweeps=400):
-    """Time the oracle (as it stands) on a bounded sample: 1 random vector, S sweeps."""
+def oracle_sample(rp, col, val, a, b, n, nnz, threads, target_s=15.0, max_sweeps=400):
+    """Time the oracle (as it stands) on a bounded sample: 1 random vector, S sweeps; the fixed
+    per-call cost (serial Z4 fill, allocation) is measured with a 1-sweep call and subtracted."""
     import oracle
 
-    threads = host_cores()
-    oracle.kpm_eta(rp, col, val, a, b, 4, 1, SEED, threads=threads)  # warm-up (threads, page faults)
-    t0 = time.perf_counter()
-    oracle.kpm_eta(rp, col, val, a, b, 8, 1, SEED, threads=threads)  # 4 sweeps, calibrate
-    t_cal = (time.perf_counter() - t0) / 4
-    sweeps = int(max(2, min(max_sweeps, target_s / max(t_cal, 1e-6))))
-    t0 = time.perf_counter()
-    oracle.kpm_eta(rp, col, val, a, b, 2 * sweeps, 1, SEED, threads=threads)
-    t = time.perf_counter() - t0
+    def call(sweeps):
+        t0 = time.perf_counter()
+        oracle.kpm_eta(rp, col, val, a, b, 2 * sweeps, 1, SEED, threads=threads)
+        return time.perf_counter() - t0
+
+    call(2)  # warm-up (threads, page faults)
+    t1, t3 = call(1), call(3)
+    t_sweep = max((t3 - t1) / 2, 1e-6)
+    setup = max(t1 - t_sweep, 0.0)
+    sweeps = int(max(2, min(max_sweeps, target_s / t_sweep)))
+    t = call(sweeps) - setup
     gf = sweeps * alg_flops_per_sweep(n, nnz, 1) / t / 1e9
-    return gf, threads, sweeps, t
+    return gf, sweeps, t, setup
 
 
 def workload(args, world):
@@ -179,6 +167,29 @@ def workload(args, world):
     return dict(nx=nx, ny=ny, nz=nz, px=px, M=M, R=R, scaling=scaling, name=name)
 
 
+def config_dict(w, world):
+    """config of the JSON line -- identical on both arms (driver's same_config check)."""
+    return {"workload": w["name"], "lattice": [w["nx"], w["ny"], w["nz"]], "M": w["M"], "R": w["R"],
+            "parallelism": f"x-slab dp{world}"}
+
+
+def host_copy_gbs(threads):
+    """STREAM-like host bandwidth (copy, read + write bytes) of the box's cores, for context."""
+    import torch
+
+    torch.set_num_threads(threads)
+    a = torch.ones(1 << 27, dtype=torch.float64)  # 1 GiB
+    b = torch.empty_like(a)
+    b.copy_(a)
+    best = 0.0
+    for _ in range(5):
+        t0 = time.perf_counter()
+        b.copy_(a)
+        best = max(best, 2 * a.numel() * 8 / (time.perf_counter() - t0) / 1e9)
+    del a, b
+    return best
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -192,22 +203,30 @@ def run_reference(args, rank, world):
     threads = host_cores()
     import oracle
 
-    sweeps = 8
+    # per step: one oracle call of S sweeps; its fixed cost (serial Z4 fill, vector allocation)
+    # measured with a 1-sweep call and kept under 5 % of the step by the choice of S
+    def call(sweeps):
+        t0 = time.perf_counter()
+        oracle.kpm_eta(rp, col, val, a, b, 2 * sweeps, 1, SEED, threads=threads)
+        return time.perf_counter() - t0
+
+    call(2)  # warm-up: threads, page faults
+    t1, t4 = call(1), call(4)
+    t_sweep = max((t4 - t1) / 3, 1e-6)
+    setup = max(t1 - t_sweep, 0.0)
+    budget = max(2.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))  # whole run: a few minutes
+    sweeps = int(max(2, budget / t_sweep, 20 * setup / t_sweep))
     for _ in range(args.warmup):
-        oracle.kpm_eta(rp, col, val, a, b, 2 * sweeps, 1, SEED, threads=threads)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.kpm_eta(rp, col, val, a, b, 2 * sweeps, 1, SEED, threads=threads)
-    t = time.perf_counter() - t0
+        call(max(2, sweeps // 4))
+    t = sum(call(sweeps) for _ in range(args.steps))
     value = args.steps * sweeps * alg_flops_per_sweep(lat.n, nnz, 1) / t / 1e9
     sample = (f"lattice {nx}x{ny}x{nz} (N={lat.n}, N_nz={nnz}; same row structure), 1 random vector, "
-              f"{sweeps} sweeps per step")
+              f"{sweeps} sweeps per step (fixed per-call cost {setup:.2f} s = {100 * setup / (t / args.steps):.1f} % of a step)")
     print(json.dumps({
         "impl": "reference", "metric": "augmented SpMMV Gflop/s (cplx dbl)", "value": value, "unit": "Gflop/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": w["scaling"], "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": w["name"], "lattice": [w["nx"], ny, nz], "M": w["M"], "R": w["R"],
-                   "parallelism": f"x-slab dp{world}"},
+        "config": config_dict(w, world),
         "cpu_baseline": {"value": value, "unit": "Gflop/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "Gflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -227,8 +246,9 @@ def main():
                          "global size fixed (strong scaling over N); C5: 1800x400x40 slab per GPU (~150 GB HBM), "
                          "M=4000, generated and converted on the GPU (weak scaling)")
     ap.add_argument("--chunk-order", default="auto", choices=["auto", "none", "ylines"],
-                    help="auto: y-line walks for the block-cache widths (R = 16, 32) when the slab has enough lines, "
-                         "else a y-banded order when the x-neighbour window exceeds ~32 MB (kpm_set_chunk_order)")
+                    help="auto: the library's own order (kpm.h kpm_set_chunk_order: a line walk derived from the "
+                         "matrix for the block-cache kernels and for large neighbour windows); none: storage order "
+                         "forced; ylines: the caller-side TI y-line order of round 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-r-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -293,8 +313,11 @@ def main():
         box = [kpm.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
         uid = box[0]
-    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-        os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
+    if world > 1 and "NCCL_DEBUG" not in os.environ:
+        # communicator INIT lines (ranks, NVLS/P2P transports) go to stderr with everything the
+        # native libraries print during setup (below); stdout stays the one JSON line
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     saved = os.dup(1)
     os.dup2(2, 1)  # anything the native libraries print during setup goes to stderr
     try:
@@ -309,26 +332,12 @@ def main():
     if on_device:  # the library keeps its own SELL copy; free the 37 GB CSR before the vectors
         del rp, col, val
         torch.cuda.empty_cache()
-    band = None
-    order = None
     sms = torch.cuda.get_device_properties(local).multi_processor_count
-
-    bc_ctas = {16: 2, 32: 1}  # CTAs per SM of the default block-cache feed at each width (kernels.cu)
-
-    def yline_order(r):
-        return chunk_order_ylines(lat, sms * bc_ctas[r], x0=x0, x1=x1, edges_last=world > 1)
-
-    use_lines = False
-    lines_ok = R in bc_ctas and lat.nz % 8 == 0 and (x1 - x0) * (lat.nz // 8) >= 2 * sms
-    if (args.chunk_order == "ylines" and R in bc_ctas and lat.nz % 8 == 0) or (args.chunk_order == "auto" and lines_ok):
-        # y-line walks in lock-stepped rounds: consecutive tiles of a CTA share y-neighbour blocks,
-        # which the block-cache feed keeps in shared memory, and the x-neighbour window a round
-        # keeps in L2 is a few tiles per CTA (C4: 11.04 -> 10.45 ms per sweep vs y-band)
-        use_lines = True
-        order = yline_order(R)
-    elif args.chunk_order == "auto" and 2 * lat.rows_per_plane * min(R, 32) * 16 > 32e6 and lat.nz % 8 == 0:
-        band = max(1, int(16e6 // (2 * 4 * nz * min(R, 32) * 16)))
-        order = chunk_order_yband(lat, x0, x1, band)
+    order = None
+    if args.chunk_order == "none":  # storage order forced (the identity permutation)
+        order = np.arange(ctx.sell_info().n_chunks, dtype=np.int64)
+    elif args.chunk_order == "ylines":  # round 1's caller-side y-line walk (workloads, TI-specific)
+        order = chunk_order_ylines(lat, sms * {16: 2, 32: 1}.get(R, 1), x0=x0, x1=x1, edges_last=world > 1)
 
     def apply_order():
         if order is not None:
@@ -359,38 +368,37 @@ def main():
     bytes_sweep = alg_bytes_per_sweep(n_loc, nnz_loc, R)  # per rank per launch
     achieved = bytes_sweep / (sweep * 1e-3) / 1e9
     bmin = alg_bytes_per_sweep(n, nnz, R) / alg_flops_per_sweep(n, nnz, R)
-    traffic, smem_wf = None, None
+    traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
-        tj = json.load(open(tf))
-        traffic = tj.get(f"{px}x{ny}x{nz}/R{R}")
-        smem_wf = tj.get(f"{px}x{ny}x{nz}/R{R}/smem_wavefronts")
+        traffic = json.load(open(tf)).get(f"{px}x{ny}x{nz}/R{R}")
     out = {
         "metric": "augmented SpMMV Gflop/s (cplx dbl)", "value": value, "unit": "Gflop/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": w["name"],
-                   "lattice": [nx, ny, nz], "N": n, "N_nz": nnz, "M": M, "R": R, "parallelism": f"x-slab dp{world}",
-                   "hbm_in_use_gb": round((total_b - free_b) / 1e9, 1), "kernel_variant": ctx.last_kernel(), "chunk_order": f"y-band {band}" if band else ("y-lines" if use_lines else "storage"), "halo": os.environ.get("KPM_HALO", "fused") if world > 1 else None,
-                   "l2": ("inputs larger than L2 (V, W %.2f GB each per GPU; matrix %.2f GB)" if
-                          (32 * R * n_loc + 20 * nnz_loc) > 126e6 else
-                          "L2-resident working set (V, W %.2f GB each, matrix %.2f GB; no flush)") % (
-                       16 * R * n_loc / 1e9, 20 * nnz_loc / 1e9)},
+        "config": config_dict(w, world),
+        "run": {"N": n, "N_nz": nnz, "hbm_in_use_gb": round((total_b - free_b) / 1e9, 1),
+                "kernel_variant": ctx.last_kernel(), "chunk_order": {"auto": "library default", "none": "storage (forced)",
+                                                                    "ylines": "caller y-lines"}[args.chunk_order],
+                "halo": os.environ.get("KPM_HALO", "fused") if world > 1 else None,
+                "l2": ("inputs larger than L2 (V, W %.2f GB each per GPU; matrix %.2f GB)" if
+                       (32 * R * n_loc + 20 * nnz_loc) > 126e6 else
+                       "L2-resident working set (V, W %.2f GB each, matrix %.2f GB; no flush)") % (
+                    16 * R * n_loc / 1e9, 20 * nnz_loc / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "kernel": "aug_spmmv main sweep (per GPU)", "sweep_ms": sweep,
                      "alg_bytes_per_launch": bytes_sweep, "peak_source": peak_src,
                      "B_min_bytes_per_flop": bmin, "P_mem_gflops_per_gpu": hbm / bmin,
                      "kernel_gflops_per_gpu": alg_flops_per_sweep(n_loc, nnz_loc, R) / (sweep * 1e-3) / 1e9},
         "gpu_launches": args.steps * n_blocks * ((M // 2) * (2 if world > 1 else 1) + 2),
-        "cache_roofline": cache_roofline(smem_wf, clocks.get("sm_mhz"), sweep, bytes_sweep / hbm / 1e9 * 1e3),
         "clocks": clocks,
     }
     # R sweep of the same lattice (HBM -> cache bottleneck shift), shorter M
     if not args.no_r_sweep and world == 1:
         by_r = {}
         for r in (1, 2, 4, 8, 16, 32):
-            if use_lines:  # only the block-cache widths walk y-lines; the others keep storage order
-                ctx.set_chunk_order(yline_order(r) if r in bc_ctas else None)
+            if args.chunk_order == "ylines":
+                ctx.set_chunk_order(chunk_order_ylines(lat, sms * {16: 2, 32: 1}[r]) if r in (16, 32) else None)
             ctx.moments(200, r, SEED, want_eta=False)
             ctx.moments(200, r, SEED, want_eta=False)
             sw = ctx.last_timing()[1]
@@ -421,10 +429,12 @@ def main():
         p_mem = hbm / bmin
         p_llc = out["cache_resident"]["gflops"]
         kern = out["roofline"]["kernel_gflops_per_gpu"]
-        out["custom_roofline"] = {"P_mem_gflops": p_mem, "P_llc_gflops": p_llc, "applicable_gflops": min(p_mem, p_llc),
-                                  "bound": "llc" if p_llc < p_mem else "hbm", "kernel_gflops": kern,
-                                  "frac": kern / min(p_mem, p_llc),
-                                  "model": "P* = min(P*_MEM, P*_LLC), Eq. (11) eq:roofline_custom, P:704"}
+        out["custom_roofline"] = {"P_mem_gflops": p_mem, "P_llc_gflops_lower_bound": p_llc,
+                                  "kernel_gflops": kern, "kernel_over_llc_lower_bound": kern / p_llc,
+                                  "model": "P* = min(P*_MEM, P*_LLC), Eq. (11) eq:roofline_custom, P:704",
+                                  "note": "context only: P*_LLC here is the kernel's own rate on a 28-us, L2-resident "
+                                          "problem, a LOWER bound of the cache ceiling (P:741-743), so this is not a "
+                                          "roofline fraction; the HBM fraction in `roofline` is the headline"}
     # e2e: host CSR in, mu/eta out, through the C ABI, copies inside the timed region
     if not args.no_e2e and on_device:
         out["e2e"] = None
@@ -453,9 +463,16 @@ def main():
                       "ms_per_step": te / args.steps, "set_matrix_ms_per_step": t_set,
                       "note": "kpm_set_matrix(host CSR: validation, SELL build, H2D) + kpm_moments (D2H mu, eta)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not on_device:
-        gf, threads, sweeps, t = oracle_sample(rp, col, val, a, b, n, nnz)
-        out["cpu_baseline"] = {"value": gf, "unit": "Gflop/s", "cores": threads, "kind": "oracle",
-                               "sample": f"same lattice, 1 random vector, {sweeps} sweeps ({t:.1f} s)"}
+        cores = host_cores()
+        gf, sweeps, t, setup = oracle_sample(rp, col, val, a, b, n, nnz, cores)
+        gf1, sweeps1, t1, _ = oracle_sample(rp, col, val, a, b, n, nnz, 1, target_s=6.0)
+        out["cpu_baseline"] = {"value": gf, "unit": "Gflop/s", "cores": cores, "kind": "oracle",
+                               "sample": f"same lattice, 1 random vector, {sweeps} sweeps ({t:.1f} s, fixed per-call "
+                                         f"cost {setup:.2f} s excluded)",
+                               "value_1_core": gf1, "sample_1_core": f"{sweeps1} sweeps ({t1:.1f} s)",
+                               "host_copy_gbs": host_copy_gbs(cores),
+                               "host_cpu": open("/proc/cpuinfo").read().split("model name")[1].split("\n")[0].strip(": ")
+                               if os.path.exists("/proc/cpuinfo") and "model name" in open("/proc/cpuinfo").read() else None}
     ctx.close()
     if rank == 0:
         print(json.dumps(out), flush=True)

@@ -85,7 +85,10 @@ enum { KPM_CHECK_HERMITIAN = 1u };
  *   an NCCL id.  Setup collectives and the final eta reduction run on the host through the
  *   group; the halo exchange is the fused one (peer stores from the edge kernels' epilogue,
  *   flag epochs) with plain device pointers in place of CUDA IPC mappings.  Every sweep kernel
- *   and the edge / interior split are the multi-GPU ones, so a single-GPU box can test them. */
+ *   and the edge / interior split are the multi-GPU ones, so a single-GPU box can test them.
+ *   Needs CUDA_DEVICE_MAX_CONNECTIONS >= 2 * nranks set before CUDA starts (every rank's stream
+ *   can block on another rank's flag; streams must not share a hardware queue), else
+ *   kpm_create returns KPM_EINVAL. */
 enum { KPM_DETERMINISTIC = 2u, KPM_TIMING = 4u, KPM_VIRTUAL_RANKS = 8u };
 
 typedef struct kpm_vgroup kpm_vgroup; /* opaque in-process rank group (KPM_VIRTUAL_RANKS) */
@@ -227,12 +230,6 @@ kpm_status kpm_export_sell(const kpm_ctx* ctx, double* val, int32_t* col, int64_
  * recv / send = NULL: only the counts; otherwise *n_recv / *n_send are the capacities (runs),
  * KPM_EINVAL if too small.  Both counts are set on return. */
 kpm_status kpm_export_halo(const kpm_ctx* ctx, int64_t* n_recv, int64_t* recv, int64_t* n_send, int64_t* send);
-
-/* Row-pair order of every SELL chunk (R18b; csrc/sell_pair.cu): n_chunks int32,
- * pinfo[c] = m | Ls << 8 -- rows a and a ^ m of chunk c (a with bit lowbit(m) clear) list the
- * Ls columns they share at entries 1..Ls; 0 = the chunk keeps the R18 order.  The exported
- * val/col arrays are in this order.  Environment KPM_PAIR=0 (read by kpm_set_matrix) skips it. */
-kpm_status kpm_export_pairs(const kpm_ctx* ctx, int32_t* pinfo);
 
 /* Host-only planning of the halo exchange (no GPU needed; the same code kpm_set_matrix
  * runs).  Row distribution: rank q owns global rows [row_begins[q], row_begins[q+1]).

@@ -17,9 +17,6 @@ Layout contract:
   * columns are renumbered: a local column i becomes invperm[i]; a column owned by
     another rank becomes n_pad + h, n_pad = n_chunks*C, h = its slot in the halo list.
   * padding slots: value 0 + 0i, column = p (the slot's own position).
-  * `pair_order` then moves, inside the rows of a chunk, the columns a row shares with its
-    partner row to the same entries 1..Ls (R18b; the product's pass is
-    csrc/sell_pair.cu).
 Halo list: all distinct remote global columns, ordered by (owner rank, global column).
 """
 from __future__ import annotations
@@ -105,58 +102,6 @@ def build_sell(row_ptr, col, val, C=32, sigma=1, row_begin=0, row_end=None, row_
         raise OverflowError("local rows + halo exceed int32")
     return dict(val=s_val, col=s_col.astype(np.int32), cptr=cptr, clen=clen.astype(np.int32),
                 perm=perm.astype(np.int32), n_pad=n_pad, halo=halo, halo_owner=halo_owner)
-
-
-def pair_order(s, C=32, max_width=32):
-    """Row-pair entry order (R18b) applied to a build_sell result, returned as a new
-    dict with the permuted val/col and `pinfo` (int32 per chunk: m | Ls << 8, 0 = unpaired).
-
-    Plain restatement of the rule, chunk by chunk with Python sets:
-      eligible chunk: 2 <= L <= max_width and every row's entry 0 is its own position;
-      for m = 1..31: rows a with bit lowbit(m) clear pair with b = a ^ m; s(a) = |distinct
-      columns != own(a), own(b) at entries >= 1 of row a| intersected with the same of row b;
-      Ls(m) = min_a s(a); keep the m of the largest Ls (first on ties); Ls = 0 -> unchanged;
-      each row: entry 0, then the Ls smallest shared columns ascending (first occurrences),
-      then its other entries in their previous order."""
-    val = s["val"].copy()
-    col = s["col"].copy()
-    cptr, clen = s["cptr"], s["clen"]
-    n_chunks = len(clen)
-    pinfo = np.zeros(n_chunks, dtype=np.int32)
-    for c in range(n_chunks):
-        L = int(clen[c])
-        if L < 2 or L > max_width:
-            continue
-        base = int(cptr[c])
-        rows = [[int(col[base + j * C + k]) for j in range(L)] for k in range(C)]
-        own = [c * C + k for k in range(C)]
-        if any(rows[k][0] != own[k] for k in range(C)):
-            continue
-
-        def shared(a, b):
-            excl = {own[a], own[b]}
-            return (set(rows[a][1:]) - excl) & (set(rows[b][1:]) - excl)
-
-        best_m, best_ls = 0, 0
-        for m in range(1, 32):
-            lb = (m & -m).bit_length() - 1
-            ls = min(len(shared(a, a ^ m)) for a in range(C) if not (a >> lb) & 1)
-            if ls > best_ls:
-                best_m, best_ls = m, ls
-        if best_ls == 0:
-            continue
-        for k in range(C):
-            cols = sorted(shared(k, k ^ best_m))[:best_ls]
-            order = [0] + [rows[k].index(g, 1) for g in cols]
-            order += [j for j in range(1, L) if j not in order]
-            src = [base + j * C + k for j in order]
-            dst = [base + j * C + k for j in range(L)]
-            val[dst] = s["val"][src]
-            col[dst] = s["col"][src]
-        pinfo[c] = best_m | (best_ls << 8)
-    out = dict(s)
-    out.update(val=val, col=col, pinfo=pinfo)
-    return out
 
 
 def sell_to_csr_entries(s, n_loc, C=32):

@@ -21,7 +21,7 @@ STATUS_NAMES = ["KPM_OK", "KPM_EINVAL", "KPM_ESTATE", "KPM_ERANGE", "KPM_ENOMEM"
                 "KPM_EZERONORM", "KPM_WDIVERGED"]
 
 # exported symbols declared in include/kpm.h
-ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_dos", "kpm_export_halo", "kpm_export_pairs", "kpm_export_sell", "kpm_get_sell_info", "kpm_get_unique_id",
+ABI_SYMBOLS = ["kpm_create", "kpm_destroy", "kpm_dos", "kpm_export_halo", "kpm_export_sell", "kpm_get_sell_info", "kpm_get_unique_id",
                "kpm_last_error", "kpm_last_kernel", "kpm_last_sweep_times", "kpm_last_timing", "kpm_moments", "kpm_moments_stage", "kpm_moments_v0",
                "kpm_plan_chunk_order", "kpm_plan_recv", "kpm_plan_send", "kpm_set_chunk_order", "kpm_set_matrix", "kpm_sweep_kernel", "kpm_variant_name", "kpm_vgroup_create",
                "kpm_vgroup_destroy"]
@@ -72,7 +72,6 @@ def load_library():
     lib.kpm_last_timing.argtypes = [P, P, P, P]
     lib.kpm_get_sell_info.argtypes = [P, ctypes.POINTER(kpm_sell_info)]
     lib.kpm_export_sell.argtypes = [P, P, P, P, P, P]
-    lib.kpm_export_pairs.argtypes = [P, P]
     lib.kpm_export_halo.argtypes = [P, P, P, P, P]
     lib.kpm_last_sweep_times.argtypes = [P, P, P]
     lib.kpm_vgroup_create.argtypes = [i32, ctypes.POINTER(P)]
@@ -329,12 +328,6 @@ class KpmContext:
         halo = np.zeros(max(info.n_halo, 1), dtype=np.int64)
         self._check(self.lib.kpm_export_sell(self.h, _ptr(val), _ptr(col), _ptr(cptr), _ptr(perm), _ptr(halo)))
         return dict(val=val, col=col, cptr=cptr, perm=perm, halo=halo[: info.n_halo], n_pad=info.n_pad)
-
-    def export_pairs(self):
-        """kpm_export_pairs: per chunk m | Ls << 8 of the row-pair order (0 = unpaired)."""
-        pinfo = np.zeros(max(self.sell_info().n_chunks, 1), dtype=np.int32)
-        self._check(self.lib.kpm_export_pairs(self.h, _ptr(pinfo)))
-        return pinfo[: self.sell_info().n_chunks]
 
     def close(self):
         if getattr(self, "h", None):

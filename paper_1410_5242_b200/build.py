@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libkpm.so")
-SOURCES = ["kernels.cu", "kpm_abi.cu", "sell_build.cpp", "halo_plan.cpp", "plan_abi.cpp", "chunk_order.cpp", "dos.cpp", "sell_device.cu", "sell_pair.cu", "naive.cu", "hermitian.cpp"]
+SOURCES = ["kernels.cu", "kpm_abi.cu", "sell_build.cpp", "halo_plan.cpp", "plan_abi.cpp", "chunk_order.cpp", "dos.cpp", "sell_device.cu", "naive.cu", "hermitian.cpp"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

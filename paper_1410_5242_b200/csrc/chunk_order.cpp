@@ -97,11 +97,17 @@ std::vector<int64_t> line_order(int64_t n_chunks, const std::vector<int64_t>& pt
   return order;
 }
 
-int64_t max_block_offset(int64_t n_chunks, const std::vector<int64_t>& ptr, const std::vector<int64_t>& nbr) {
-  int64_t m = 0;
-  for (int64_t c = 0; c < n_chunks; ++c)
+int64_t typical_block_offset(int64_t n_chunks, const std::vector<int64_t>& ptr, const std::vector<int64_t>& nbr) {
+  std::vector<int64_t> per;  // largest |b - c| of every chunk that has block neighbours
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    int64_t m = -1;
     for (int64_t i = ptr[c]; i < ptr[c + 1]; ++i) m = std::max(m, nbr[i] > c ? nbr[i] - c : c - nbr[i]);
-  return m;
+    if (m >= 0) per.push_back(m);
+  }
+  if (per.empty()) return 0;
+  // the 90th percentile: a periodic wrap (the first plane's neighbours in the last) is rare
+  std::nth_element(per.begin(), per.begin() + (int64_t)(per.size() * 9 / 10), per.end());
+  return per[per.size() * 9 / 10];
 }
 
 }  // namespace kpm

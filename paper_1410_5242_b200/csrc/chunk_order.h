@@ -17,7 +17,8 @@ void block_neighbours(int64_t n_chunks, const int* nruns, const int* runs, int m
 std::vector<int64_t> line_order(int64_t n_chunks, const std::vector<int64_t>& ptr, const std::vector<int64_t>& nbr,
                                 int64_t G, const std::vector<char>& skip);
 
-// Largest |b - c| over block-neighbour pairs (the neighbour window of a storage-order sweep).
-int64_t max_block_offset(int64_t n_chunks, const std::vector<int64_t>& ptr, const std::vector<int64_t>& nbr);
+// 90th percentile over the chunks of the largest |b - c| to a block neighbour: the reuse distance
+// (in chunks) of a storage-order sweep, periodic wraps aside.
+int64_t typical_block_offset(int64_t n_chunks, const std::vector<int64_t>& ptr, const std::vector<int64_t>& nbr);
 
 }  // namespace kpm

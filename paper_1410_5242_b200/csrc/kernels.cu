@@ -682,270 +682,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
   }
 }
 
-// ------------------------------------------------------------- row-pair feed -------
-// DESIGN.md §7 "Row-pair feed" (experiment).  The shared-memory data path delivers 128 B per clock
-// per SM to registers whatever the number of distinct addresses, so the per-lane bytes loaded per
-// complex FMA bound the R = 32 sweep (4 wavefronts of V plus 1 of the value per row entry at 8
-// lanes per row).  Here a lane owns 4 block columns of TWO rows a, b = a ^ m of its chunk
-// (sell_pair.cu orders their entries so that the Ls columns they share sit at entries 1..Ls of
-// both rows): one V load then feeds both rows' accumulators (TI: 9 instead of 13 V reads per
-// row).  A chunk is 16 pairs = 4 warps; one group of 4 consumer warps and the producer warp of
-// the block-cache feed (same records, W staged, 2-stage ring), so the pool behaves exactly as in
-// aug_spmmv_tiled's BC variant.
-template <int R>
-struct PairCfg {
-  static constexpr int CPL = 4;          // block columns per lane
-  static constexpr int LPR = R / CPL;    // lanes per pair
-  static constexpr int PW = 32 / LPR;    // pairs per warp
-  static constexpr int NCW = 16 / PW;    // consumer warps (16 pairs per chunk)
-  static constexpr int THREADS = 32 * (NCW + 1);
-  static_assert(LPR == 8, "row-pair feed: R = 32");
-};
-constexpr int kMaxPairStages = 4;
-
-// One row's epilogue: -b V_i, x 2a (a at init), - W_old, streaming store (+ peer copy), dots.
-template <int R, bool INIT>
-__device__ __forceinline__ void pair_finish(const SweepArgs& a, int64_t p, const double2 (&u)[4],
-                                            const double2 (&x0)[4], bool own0, const double2* own_v,
-                                            const double2* w_old, int t, uint64_t pol, Dots<4>& d) {
-  constexpr int LPR = PairCfg<R>::LPR;
-  if (p >= a.n_loc) return;
-#pragma unroll
-  for (int cc = 0; cc < 4; ++cc) {
-    const int col = cc * LPR + t;
-    const double2 vi = own0 ? x0[cc] : own_v[col];
-    double2 uu = u[cc];
-    uu.x = fma(-a.b, vi.x, uu.x);
-    uu.y = fma(-a.b, vi.y, uu.y);
-    double2 w;
-    if (INIT) {
-      w = make_double2(a.scale * uu.x, a.scale * uu.y);
-    } else {
-      const double2 wo = w_old[col];
-      w = make_double2(fma(a.scale, uu.x, -wo.x), fma(a.scale, uu.y, -wo.y));
-    }
-    st_stream(a.W + p * R + col, w, pol);
-    store_peers<R>(a, p, col, w);
-    d.ee[cc] = fma(vi.x, vi.x, fma(vi.y, vi.y, d.ee[cc]));
-    d.eor[cc] = fma(w.x, vi.x, fma(w.y, vi.y, d.eor[cc]));
-    d.eoi[cc] = fma(w.x, vi.y, fma(-w.y, vi.x, d.eoi[cc]));
-  }
-}
-
-template <int R, bool INIT, int U, int U2>
-__global__ void __launch_bounds__(PairCfg<R>::THREADS, 1) aug_spmmv_pair(const SweepArgs a) {
-  using PC = PairCfg<R>;
-  constexpr int CPL = PC::CPL, LPR = PC::LPR, PW = PC::PW, NCW = PC::NCW;
-  extern __shared__ __align__(128) unsigned char tsm[];
-  __shared__ __align__(8) uint64_t full[kMaxPairStages], empty[kMaxPairStages];
-  __shared__ int tile_hdr[kMaxPairStages], tile_own[kMaxPairStages];
-  __shared__ int64_t tile_chunk[kMaxPairStages];
-  __shared__ double red[NCW * 3 * R];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const TileLayout tl = a.tl;
-  const int S = tl.stages;
-  const int64_t n_chunks = a.chunk_end - a.chunk_begin;
-  const int64_t my_tiles = n_chunks > blockIdx.x ? (n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const uint64_t pol = policy_evict_first();
-
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), NCW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  Dots<CPL> d;
-  d.zero();
-  if (warp == NCW) {
-    // ---------------- producer warp (as in aug_spmmv_tiled's block-cache feed) --------------
-    const uint64_t pol_v = a.v_evict_last ? policy_evict_last() : 0ull;
-    int64_t c_nxt = my_tiles > 0 ? chunk_at(a, blockIdx.x) : 0;
-    uint4 nxt = my_tiles > 0 && lane < 16 ? __ldg(a.rec + (int64_t)blockIdx.x * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
-    for (int64_t k = 0; k < my_tiles; ++k) {
-      const uint4 cur = nxt;
-      const int64_t c_cur = c_nxt;
-      if (k + 1 < my_tiles) {
-        c_nxt = chunk_at(a, blockIdx.x + (k + 1) * gridDim.x);
-        nxt = lane < 16 ? __ldg(a.rec + (blockIdx.x + (k + 1) * gridDim.x) * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
-      }
-      const int s = (int)(k % S);
-      const uint32_t total = __shfl_sync(0xffffffffu, INIT ? cur.y : cur.x, 0);
-      const uint32_t hz = __shfl_sync(0xffffffffu, cur.z, 0);
-      const uint32_t hw = __shfl_sync(0xffffffffu, cur.w, 0);
-      const uint32_t ncmd = hw & 0xFFu;
-      if (k >= S) mbar_wait(smem_u32(&empty[s]), (uint32_t)(((k / S) - 1) & 1));
-      const uint32_t bar = smem_u32(&full[s]);
-      if (lane == 0) {
-        tile_hdr[s] = (int)hz;
-        tile_own[s] = (int)((hw >> 8) & 0xFFFFu);
-        tile_chunk[s] = c_cur;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_expect_tx(bar, total);
-      }
-      __syncwarp();
-      if (lane >= 1 && (uint32_t)lane <= ncmd) {
-        const uint32_t base = cur.w >> 28, bytes = cur.w & 0x0FFFFFFFu;
-        const int64_t off = (int64_t)(((uint64_t)cur.y << 32) | cur.x);
-        if (!INIT || base != 1) {
-          const unsigned char* src = base == 0   ? reinterpret_cast<const unsigned char*>(a.V)
-                                     : base == 1 ? reinterpret_cast<const unsigned char*>(a.W)
-                                     : base == 2 ? reinterpret_cast<const unsigned char*>(a.val)
-                                                 : reinterpret_cast<const unsigned char*>(a.lcol);
-          bulk_g2s(smem_u32(tsm + cur.z), src + off, bytes, bar, base == 0 ? pol_v : pol);
-        }
-      }
-    }
-  } else {
-    // ---------------- consumer warps ---------------------------------------------------
-    const int q = lane / LPR, t = lane - q * LPR;
-    const int i = warp * PW + q;  // pair of the chunk
-    const double2* sVt = reinterpret_cast<const double2*>(tsm) + t;
-    for (int64_t k = 0; k < my_tiles; ++k) {
-      const int s = (int)(k % S);
-      const unsigned char* st = tsm + (size_t)tl.pool_bytes + (size_t)s * tl.stage_bytes;
-      const double2* sW = reinterpret_cast<const double2*>(st + tl.off_w);
-      const double2* sval = reinterpret_cast<const double2*>(st + tl.off_val);
-      const uint16_t* slc = reinterpret_cast<const uint16_t*>(st + tl.off_lcol);
-      mbar_wait(smem_u32(&full[s]), (uint32_t)((k / S) & 1));
-      const int hdr = tile_hdr[s];
-      const int L = hdr & 0xFFFF, Ls = (hdr >> 16) & 0xFF, m = (hdr >> 24) & 0x1F;
-      const int own_row = tile_own[s];
-      const int64_t c = tile_chunk[s];
-      int ra, rb;
-      if (m) {
-        const int lb = __ffs(m) - 1;
-        ra = ((i >> lb) << (lb + 1)) | (i & ((1 << lb) - 1));
-        rb = ra ^ m;
-      } else {
-        ra = 2 * i;
-        rb = ra + 1;
-      }
-      double2 ua[CPL], ub[CPL], xa0[CPL], xb0[CPL];
-#pragma unroll
-      for (int cc = 0; cc < CPL; ++cc) ua[cc] = ub[cc] = xa0[cc] = xb0[cc] = make_double2(0.0, 0.0);
-      int lia0 = -1, lib0 = -1;
-      // entry 0: the row's own position (R18 / R18b), its gather doubles as the epilogue's V_i
-      if (L > 0) {
-        const double2 ha = sval[ra], hb = sval[rb];
-        lia0 = slc[ra] * R;
-        lib0 = slc[rb] * R;
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-          xa0[cc] = sVt[lia0 + cc * LPR];
-          xb0[cc] = sVt[lib0 + cc * LPR];
-          cmac(ua[cc], ha, xa0[cc]);
-          cmac(ub[cc], hb, xb0[cc]);
-        }
-      }
-      const bool own_a = lia0 == (own_row + ra) * R, own_b = lib0 == (own_row + rb) * R;
-      // entries 1..Ls: columns both rows list, one V load for both
-      int j = 1;
-      for (; j + U <= Ls + 1; j += U) {
-        double2 ha[U], hb[U];
-        int li[U];
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-          ha[uu] = sval[(j + uu) * kC + ra];
-          hb[uu] = sval[(j + uu) * kC + rb];
-          li[uu] = slc[(j + uu) * kC + ra] * R;
-        }
-        double2 x[U][CPL];
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu)
-#pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) x[uu][cc] = sVt[li[uu] + cc * LPR];
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu)
-#pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) {
-            cmac(ua[cc], ha[uu], x[uu][cc]);
-            cmac(ub[cc], hb[uu], x[uu][cc]);
-          }
-      }
-      for (; j <= Ls; ++j) {
-        const double2 ha = sval[j * kC + ra], hb = sval[j * kC + rb];
-        const int li = slc[j * kC + ra] * R;
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-          const double2 x = sVt[li + cc * LPR];
-          cmac(ua[cc], ha, x);
-          cmac(ub[cc], hb, x);
-        }
-      }
-      // the remaining entries of each row
-      for (; j + U2 <= L; j += U2) {
-        double2 ha[U2], hb[U2];
-        int la[U2], lb2[U2];
-#pragma unroll
-        for (int uu = 0; uu < U2; ++uu) {
-          ha[uu] = sval[(j + uu) * kC + ra];
-          hb[uu] = sval[(j + uu) * kC + rb];
-          la[uu] = slc[(j + uu) * kC + ra] * R;
-          lb2[uu] = slc[(j + uu) * kC + rb] * R;
-        }
-        double2 xa[U2][CPL], xb[U2][CPL];
-#pragma unroll
-        for (int uu = 0; uu < U2; ++uu)
-#pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) {
-            xa[uu][cc] = sVt[la[uu] + cc * LPR];
-            xb[uu][cc] = sVt[lb2[uu] + cc * LPR];
-          }
-#pragma unroll
-        for (int uu = 0; uu < U2; ++uu)
-#pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) {
-            cmac(ua[cc], ha[uu], xa[uu][cc]);
-            cmac(ub[cc], hb[uu], xb[uu][cc]);
-          }
-      }
-      for (; j < L; ++j) {
-        const double2 ha = sval[j * kC + ra], hb = sval[j * kC + rb];
-        const int la = slc[j * kC + ra] * R, lb = slc[j * kC + rb] * R;
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-          cmac(ua[cc], ha, sVt[la + cc * LPR]);
-          cmac(ub[cc], hb, sVt[lb + cc * LPR]);
-        }
-      }
-      const double2* sV = reinterpret_cast<const double2*>(tsm);
-      pair_finish<R, INIT>(a, c * kC + ra, ua, xa0, own_a, sV + (own_row + ra) * R, sW + ra * R, t, pol, d);
-      pair_finish<R, INIT>(a, c * kC + rb, ub, xb0, own_b, sV + (own_row + rb) * R, sW + rb * R, t, pol, d);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&empty[s]));  // stage s released by this warp
-    }
-#pragma unroll
-    for (int off = LPR; off < 32; off <<= 1) {
-#pragma unroll
-      for (int cc = 0; cc < CPL; ++cc) {
-        d.ee[cc] += __shfl_xor_sync(0xffffffffu, d.ee[cc], off);
-        d.eor[cc] += __shfl_xor_sync(0xffffffffu, d.eor[cc], off);
-        d.eoi[cc] += __shfl_xor_sync(0xffffffffu, d.eoi[cc], off);
-      }
-    }
-    if (lane < LPR) {
-#pragma unroll
-      for (int cc = 0; cc < CPL; ++cc) {
-        const int r = cc * LPR + t;
-        red[warp * 3 * R + r] = d.ee[cc];
-        red[warp * 3 * R + R + r] = d.eor[cc];
-        red[warp * 3 * R + 2 * R + r] = d.eoi[cc];
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < 3 * R; i += PC::THREADS) {
-    double sum = 0.0;
-#pragma unroll
-    for (int w = 0; w < NCW; ++w) sum += red[w * 3 * R + i];
-    a.partials[(int64_t)i * a.pstride + blockIdx.x] = sum;
-  }
-}
-
-enum Feed { kDirect = 0, kStaged = 1, kTiled = 2, kPair = 3 };
+enum Feed { kDirect = 0, kStaged = 1, kTiled = 2 };
 
 template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true, int MINB = 1, bool BC = false>
 struct Variant {
@@ -985,26 +722,6 @@ struct Variant {
   }
 };
 
-template <int R, int U, int U2>
-struct PairVariant {
-  static cudaError_t launch(bool init, const SweepArgs& a, int grid, cudaStream_t s) {
-    const int smem = a.tl.pool_bytes + a.tl.stages * a.tl.stage_bytes;
-    auto k_init = aug_spmmv_pair<R, true, U, U2>;
-    auto k_main = aug_spmmv_pair<R, false, U, U2>;
-    cudaFuncSetAttribute(k_init, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    (init ? k_init : k_main)<<<grid, PairCfg<R>::THREADS, smem, s>>>(a);
-    return cudaGetLastError();
-  }
-  static int occupancy(int dyn_smem) {
-    int n = 0;
-    auto k_main = aug_spmmv_pair<R, false, U, U2>;
-    cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_main, PairCfg<R>::THREADS, dyn_smem);
-    return n;
-  }
-};
-
 typedef cudaError_t (*LaunchFn)(bool, const SweepArgs&, int, cudaStream_t);
 typedef int (*OccFn)(int);
 struct Entry {
@@ -1016,10 +733,7 @@ struct Entry {
   OccFn occ;
   int stages = 0;  // tiled feed: preferred ring depth (0 = plan_tiles default)
   int bc_ctas = 0;  // block-cache feed: CTAs per SM its shared-memory plan is sized for (0: not BC)
-  int pair = 0;     // row-pair feed (1): block-cache records with the chunk's pair order in the header
 };
-#define KPM_VARIANT_PAIR(R, U, U2, NAME)                                                                  \
-  {R, NAME, kPair, true, PairVariant<R, U, U2>::launch, PairVariant<R, U, U2>::occupancy, 2, 1, 1}
 #define KPM_VARIANT(R, LPR, U, F, NAME) {R, NAME, F, true, Variant<R, LPR, U, F>::launch, Variant<R, LPR, U, F>::occupancy}
 #define KPM_VARIANT_CS(R, LPR, U, CS, NAME) \
   {R, NAME, kTiled, true, Variant<R, LPR, U, kTiled, CS>::launch, Variant<R, LPR, U, kTiled, CS>::occupancy}
@@ -1031,8 +745,10 @@ struct Entry {
 #define KPM_VARIANT_WR(R, LPR, U, NAME) \
   {R, NAME, kTiled, false, Variant<R, LPR, U, kTiled, 1, false>::launch, Variant<R, LPR, U, kTiled, 1, false>::occupancy}
 // First entry of each width is the default (chosen from the B200 measurements in DESIGN.md); at
-// R = 16 and 32 that is the block-cache feed, single rank only, and the first other entry
-// (base_variant) is what runs where it cannot (several ranks, a plan that does not fit).
+// R = 16 and 32 that is the block-cache feed (on one rank: one plan for the chunk order; on several
+// ranks: one plan per edge / interior list).  Where its plan does not fit the matrix on some rank,
+// every rank falls back together to the next variant in table order that fits (select_variant in
+// kpm_abi.cu); the last entry of each width, the direct feed, always does.
 const Entry kTable[] = {
     KPM_VARIANT(1, 1, 4, kTiled, "tiled.lpr1.u4"),
     KPM_VARIANT(1, 1, 4, kDirect, "direct.lpr1.u4"),
@@ -1058,6 +774,8 @@ const Entry kTable[] = {
     {16, "tiled.bc.lpr4.u4.wr", kTiled, false, Variant<16, 4, 4, kTiled, 1, false, 2, true>::launch,
      Variant<16, 4, 4, kTiled, 1, false, 2, true>::occupancy, 2, 2},
     KPM_VARIANT_WR_S(16, 4, 4, 2, "tiled.lpr4.u4.wr.s2"),
+    {16, "tiled.bc.lpr8.u4.wr", kTiled, false, Variant<16, 8, 4, kTiled, 1, false, 2, true>::launch,
+     Variant<16, 8, 4, kTiled, 1, false, 2, true>::occupancy, 2, 2},
     KPM_VARIANT(16, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(16, 4, 2, kTiled, "tiled.lpr4.u2"),
     KPM_VARIANT_WR(16, 8, 4, "tiled.lpr8.u4.wr"),
@@ -1068,9 +786,6 @@ const Entry kTable[] = {
     KPM_VARIANT(16, 8, 4, kDirect, "direct.lpr8.u4"),
     {32, "tiled.bc.lpr8.u4", kTiled, true, Variant<32, 8, 4, kTiled, 1, true, 1, true>::launch,
      Variant<32, 8, 4, kTiled, 1, true, 1, true>::occupancy, 2, 1},
-    KPM_VARIANT_PAIR(32, 2, 1, "pair.bc.lpr8.u2"),
-    KPM_VARIANT_PAIR(32, 4, 1, "pair.bc.lpr8.u4"),
-    KPM_VARIANT_PAIR(32, 4, 2, "pair.bc.lpr8.u4.v2"),
     KPM_VARIANT(32, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT_WR(32, 8, 4, "tiled.lpr8.u4.wr"),
     KPM_VARIANT_CS(32, 8, 4, 2, "tiled.lpr8.u4.cs2"),
@@ -1106,7 +821,7 @@ bool variant_staged(int R, int variant) {
 
 bool variant_tiled(int R, int variant) {
   const Entry* e = find(R, variant);
-  return e && (e->feed == kTiled || e->feed == kPair);
+  return e && e->feed == kTiled;
 }
 
 int variant_stages(int R, int variant) {
@@ -1122,11 +837,6 @@ int base_variant(int R) {
       ++i;
     }
   return 0;
-}
-
-int variant_pair(int R, int variant) {
-  const Entry* e = find(R, variant);
-  return e ? e->pair : 0;
 }
 
 int variant_bc(int R, int variant) {
@@ -1164,7 +874,7 @@ TileLayout plan_tiles(int R, int64_t max_other, int64_t max_width, int stages, b
 // pool takes the rest of the budget in 32-row blocks: at least 5 S, so that S tiles without
 // any reuse (TI: own + 4 neighbour blocks each) can be in flight.
 constexpr int kBcExtraRows = 8;
-TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas, int min_slots) {
+TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas) {
   TileLayout tl;
   const int64_t rowb = 16ll * R;
   const int S = stages > 0 ? stages : 2;
@@ -1175,7 +885,7 @@ TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int 
   const int64_t stage = up(extra + w + val + lc);
   const int64_t pool = kTileBudget / std::max(ctas, 1) - (ctas > 1 ? 4096 : 0) - S * stage;
   const int P = (int)std::min<int64_t>(kBcMaxSlots, pool / (kC * rowb));
-  if (P < (min_slots > 0 ? min_slots : 5 * S)) return tl;
+  if (P < 5 * S) return tl;
   tl.stages = S;
   tl.stage_bytes = (int)stage;
   tl.off_w = (int)extra;

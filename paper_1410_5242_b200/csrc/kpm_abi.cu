@@ -120,7 +120,7 @@ struct kpm_ctx {
   std::map<int64_t, std::vector<int64_t>> auto_order;  // line walk per grid (chunk_order.cpp)
   int adj_state = 0;                // block-neighbour lists: 0 not built, 1 built, -1 unavailable
   std::vector<int64_t> adj_ptr, adj;
-  int64_t adj_maxoff = 0;
+  int64_t adj_maxoff = 0;          // typical_block_offset of the matrix (chunks)
   int64_t* halo_rows = nullptr;     // device: global id of each halo slot
   // fused halo exchange (peer stores from the sweep epilogue + stream flag ops)
   bool fused = false;               // chosen per set_matrix (env KPM_HALO=nccl|fused)
@@ -211,6 +211,17 @@ extern "C" kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt) {
   if (virt && (!opt->nccl_unique_id || static_cast<const kpm_vgroup*>(opt->nccl_unique_id)->P != opt->nranks)) {
     g_create_err = "KPM_VIRTUAL_RANKS needs nccl_unique_id = a kpm_vgroup of nranks ranks";
     return KPM_EINVAL;
+  }
+  if (virt && opt->nranks > 1) {
+    // every virtual rank's stream may block in cuStreamWaitValue32 on another rank's flag; with
+    // fewer hardware queues than streams two ranks could share one and deadlock
+    const char* mc = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    if (!mc || atoi(mc) < 2 * opt->nranks) {
+      g_create_err = "KPM_VIRTUAL_RANKS with nranks = " + std::to_string(opt->nranks) +
+                     " needs CUDA_DEVICE_MAX_CONNECTIONS >= " + std::to_string(2 * opt->nranks) +
+                     " in the environment before CUDA starts (one hardware queue per stream)";
+      return KPM_EINVAL;
+    }
   }
   if (opt->flags & ~(unsigned)(KPM_CHECK_HERMITIAN | KPM_DETERMINISTIC | KPM_TIMING | KPM_VIRTUAL_RANKS)) {
     g_create_err = "unknown kpm_options.flags bits";
@@ -372,7 +383,6 @@ static void free_sell(DevSell& s) {
   cudaFree(s.lcol);
   cudaFree(s.nruns);
   cudaFree(s.runs);
-  cudaFree(s.pinfo);
   for (int i = 0; i < 12; ++i) cudaFree(s.rec[i]);
   s = DevSell();
 }
@@ -383,7 +393,6 @@ static void reset_sell(DevSell& s) {
   k.val = s.val, k.col = s.col, k.cptr = s.cptr, k.perm_buf = s.perm_buf, k.lcol = s.lcol, k.nruns = s.nruns, k.runs = s.runs;
   k.val_cap = s.val_cap, k.col_cap = s.col_cap, k.cptr_cap = s.cptr_cap, k.perm_cap = s.perm_cap;
   k.lcol_cap = s.lcol_cap, k.nruns_cap = s.nruns_cap, k.runs_cap = s.runs_cap;
-  k.pinfo = s.pinfo, k.pinfo_cap = s.pinfo_cap;
   for (int i = 0; i < 12; ++i) {
     k.rec[i] = s.rec[i];
     k.rec_cap[i] = s.rec_cap[i];
@@ -518,7 +527,7 @@ static kpm_status ensure_adjacency(kpm_ctx* ctx) {
   KPM_CUDA(cudaMemcpy(nr.data(), s.nruns, sizeof(int) * nr.size(), cudaMemcpyDeviceToHost));
   KPM_CUDA(cudaMemcpy(rr.data(), s.runs, sizeof(int) * rr.size(), cudaMemcpyDeviceToHost));
   block_neighbours(s.n_chunks, nr.data(), rr.data(), kMaxRuns, kC, ctx->adj_ptr, ctx->adj);
-  ctx->adj_maxoff = max_block_offset(s.n_chunks, ctx->adj_ptr, ctx->adj);
+  ctx->adj_maxoff = typical_block_offset(s.n_chunks, ctx->adj_ptr, ctx->adj);
   ctx->adj_state = 1;
   return KPM_OK;
 }
@@ -530,7 +539,9 @@ static kpm_status ensure_order(kpm_ctx* ctx, int64_t grid, bool bc_kernel, int R
   if (ctx->order_user) return install_order(ctx, ctx->order_h, -1);
   kpm_status st = ensure_adjacency(ctx);
   if (st != KPM_OK) return st;
-  const bool big_window = ctx->adj_state == 1 && (double)ctx->adj_maxoff * kC * Rk * 16.0 > 32e6;
+  // V rows a storage-order sweep must keep in L2 between a row's first and last use: both sides
+  // of the reuse distance (TI: two x-planes; C4 at R = 32: 65.5 MB, C3: 16.4 MB)
+  const bool big_window = ctx->adj_state == 1 && 2.0 * (double)ctx->adj_maxoff * kC * Rk * 16.0 > 32e6;
   if (ctx->adj_state == 1 && (bc_kernel || big_window) && env_int("KPM_AUTO_ORDER", 1)) {
     std::vector<int64_t>& o = ctx->auto_order[grid];
     if (o.empty()) {
@@ -785,17 +796,6 @@ extern "C" kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, d
             }
       }
     }
-    // a0, last step: row-pair entry order (R18b), on the device for both build paths
-    if (reserve((void**)&d.pinfo, &d.pinfo_cap, sizeof(int) * std::max<int64_t>(1, d.n_chunks)) != cudaSuccess) {
-      cudaGetLastError();
-      reset_sell(ctx->sell);
-      return fail(ctx, KPM_ENOMEM, "device allocation for the pair plan failed");
-    }
-    if (env_int("KPM_PAIR", 1)) {
-      KPM_CUDA(launch_pair_order(d.cptr, d.n_chunks, d.val, d.col, d.tiles_ok ? d.lcol : nullptr, d.pinfo, ctx->stream));
-    } else {
-      KPM_CUDA(cudaMemsetAsync(d.pinfo, 0, sizeof(int) * std::max<int64_t>(1, d.n_chunks), ctx->stream));
-    }
     KPM_CUDA(cudaStreamSynchronize(ctx->stream));
     return KPM_OK;
   };
@@ -1005,10 +1005,8 @@ static kpm_status plan_tiled_feed(kpm_ctx* ctx, int Rk, bool with_w, int pref_st
 // this grid and chunk order, built once and cached under bc_key.  ok = every tile fits.
 static kpm_status build_bc_plan(kpm_ctx* ctx, int Rk, int v, const TileLayout& tl, int grid, bool& ok) {
   const DevSell& s = ctx->sell;
-  const bool pair = variant_pair(Rk, v) > 0;
   const bool wst = variant_wstage(Rk, v);
-  const std::vector<int64_t> key = {Rk, grid, ctx->matrix_gen, ctx->order_gen, tl.stages, wst ? 1 : 0, pair ? 1 : 0,
-                                    tl.pool_slots};
+  const std::vector<int64_t> key = {Rk, grid, ctx->matrix_gen, ctx->order_gen, tl.stages, wst ? 1 : 0, tl.pool_slots};
   if (key == ctx->bc_key) {
     ok = ctx->bc_ok;
     return KPM_OK;
@@ -1030,18 +1028,16 @@ static kpm_status build_bc_plan(kpm_ctx* ctx, int Rk, int v, const TileLayout& t
   KPM_CUDA(cudaMemsetAsync(ctx->bc_fail, 0, sizeof(int), ctx->stream));
   // one plan per launch list (single rank: the chunk order; several ranks: the edge and the
   // interior list, whose chunks are disjoint, so they share the lcol array)
-  const int* pinfo = pair ? s.pinfo : nullptr;
-  const int relax = 0, ng = 1;
   if (ctx->opt.nranks == 1) {
     KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->order_list, s.n_chunks, grid, Rk, wst, tl, ctx->bc_rec,
-                             ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, pinfo, relax, ng, ctx->stream));
+                             ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, ctx->stream));
   } else {
     if (ctx->n_edge)
       KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->edge_list, ctx->n_edge, grid, Rk, wst, tl,
-                               ctx->bc_rec, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, pinfo, relax, ng, ctx->stream));
+                               ctx->bc_rec, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, ctx->stream));
     if (ctx->n_interior)
       KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->interior_list, ctx->n_interior, grid, Rk, wst, tl,
-                               ctx->bc_rec2, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, pinfo, relax, ng, ctx->stream));
+                               ctx->bc_rec2, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, ctx->stream));
   }
   int hfail = 0;
   KPM_CUDA(cudaMemcpyAsync(&hfail, ctx->bc_fail, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1654,15 +1650,6 @@ extern "C" kpm_status kpm_export_sell(const kpm_ctx* ctx_c, double* val, int32_t
   if (perm && !s.perm)
     for (int64_t p = 0; p < s.n_loc; ++p) perm[p] = (int32_t)p;  // sigma = 1: identity
   if (halo && !ctx->halo.empty()) std::memcpy(halo, ctx->halo.data(), sizeof(int64_t) * ctx->halo.size());
-  return KPM_OK;
-}
-
-extern "C" kpm_status kpm_export_pairs(const kpm_ctx* ctx_c, int32_t* pinfo) {
-  kpm_ctx* ctx = const_cast<kpm_ctx*>(ctx_c);
-  if (!ctx || !pinfo) return KPM_EINVAL;
-  if (!ctx->have_matrix) return fail(ctx, KPM_ESTATE, "no matrix");
-  KPM_CUDA(cudaSetDevice(ctx->opt.device));
-  KPM_CUDA(cudaMemcpy(pinfo, ctx->sell.pinfo, sizeof(int32_t) * ctx->sell.n_chunks, cudaMemcpyDeviceToHost));
   return KPM_OK;
 }
 

@@ -43,13 +43,12 @@ struct DevSell {
   int* nruns = nullptr;        // n_chunks: runs of other rows per chunk
   int* runs = nullptr;         // n_chunks x kMaxRuns x (first row, count)
   int64_t max_other = 0, max_runs = 0;
-  int* pinfo = nullptr;        // n_chunks: row-pair order of the chunk (sell_pair.cu): m | Ls << 8, 0 = unpaired
   uint4* rec[12] = {};        // copy records per (log2(R), W staged)
   size_t rec_cap[12] = {};
   bool rec_valid[12] = {};     // built for the current matrix
   bool rec_failed[12] = {};
   // capacities (bytes) of the grow-only buffers above
-  size_t val_cap = 0, col_cap = 0, cptr_cap = 0, perm_cap = 0, lcol_cap = 0, nruns_cap = 0, runs_cap = 0, pinfo_cap = 0;
+  size_t val_cap = 0, col_cap = 0, cptr_cap = 0, perm_cap = 0, lcol_cap = 0, nruns_cap = 0, runs_cap = 0;
 };
 
 // Shared-memory layout of one stage of the tiled feed (bytes, 128-B aligned sections).
@@ -62,7 +61,7 @@ struct TileLayout {
   // starts at pool_bytes + s * stage_bytes; all offsets are multiples of one V row (16 R bytes)
   int pool_bytes = 0, pool_slots = 0, extra_rows = 0;
 };
-constexpr int kBcMaxSlots = 40;  // block-cache pool slots (max)
+constexpr int kBcMaxSlots = 16;  // block-cache pool slots (max)
 constexpr int kBcMapInts = 40;   // per tile: [n_blocks, (block, smem row) x 7, -, n_extra, (row, count, smem row) x 8]
 
 // Fused halo exchange: rows [pos, pos+count) of the new W are also stored to dst (a peer
@@ -161,22 +160,13 @@ int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val,
 // Block-cache feed: per-position copy records (kRecSlots uint4, list position b + G k = CTA b's
 // k-th tile) from a simulation of each CTA's pool of 32-row V blocks, and the tile-row index
 // of every SELL slot pointing into that CTA's shared memory.  *fail != 0 if some tile does not fit.
-// pinfo (NULL: none) goes into the record headers of the row-pair feed; relax > 0 lets a tile
-// wait for up to `relax` more releases when no pool slot is free (header bits 24..27); ng > 1:
-// the tile -> stage map of the row-pair feed's ng consumer groups (kernels.cu pair_stage).
 cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* runs, const int* scol,
                             const int64_t* list, int64_t n_chunks, int grid, int R, bool with_w,
                             const TileLayout& tl, uint4* rec, int* map, uint16_t* lcol_bc, int* fail,
-                            const int* pinfo, int relax, int ng, cudaStream_t s);
-// min_slots: smallest pool (32-row blocks) the plan accepts (0: 5 per stage)
-TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas, int min_slots = 0);
+                            cudaStream_t s);
+TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas);
 int variant_bc(int R, int variant);  // block-cache feed: CTAs per SM it is planned for, 0 = other feed
-int variant_pair(int R, int variant);  // row-pair feed: tiles in flight (consumer groups), 0 = other feed
 int base_variant(int R);             // first variant of width R that is not a block-cache feed
-// Row-pair entry order (sell_pair.cu, R18b): permutes val/col/lcol (lcol may be NULL)
-// inside the rows of every eligible chunk, pinfo[c] = m | Ls << 8 (0 = unpaired).
-cudaError_t launch_pair_order(const int64_t* cptr, int64_t n_chunks, double2* val, int* col, uint16_t* lcol,
-                              int* pinfo, cudaStream_t s);
 cudaError_t launch_build_records(const int64_t* cptr, const int* nruns, const int* runs, int64_t n_chunks, int R,
                                  int off_w, int off_val, int off_lcol, uint4* rec, cudaStream_t s);
 

@@ -281,14 +281,10 @@ __global__ void build_records_kernel(const int64_t* __restrict__ cptr, const int
 // block-aligned full 32-row run of its other rows (pool), the remaining rows are copied per
 // stage (extra rows).  A slot may be refilled for tile k only if its last user is tile k - S or
 // older: the producer refills stage k % S after all warps released tile k - S (ring order).
-// Row-pair feed (pinfo != NULL): several consumer groups hold S tiles in flight; a block no
-// free slot can take for tile k may instead wait for the release of tiles k - S + 1 .. k - S + d
-// (d <= relax, header bits 24..27: the producer waits for them before issuing tile k), which
-// only stalls the pipeline where a CTA's walk jumps (the first tiles of a new y-line).
 __global__ void bc_plan_kernel(const int64_t* __restrict__ cptr, const int* __restrict__ nruns,
                                const int* __restrict__ runs, const int64_t* __restrict__ list, int64_t n_chunks, int G,
                                int R, int with_w, TileLayout tl, uint4* __restrict__ rec, int* __restrict__ map,
-                               int* __restrict__ fail, const int* __restrict__ pinfo, int relax, int ng) {
+                               int* __restrict__ fail) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= G) return;
   int sblk[kBcMaxSlots];
@@ -302,10 +298,7 @@ __global__ void bc_plan_kernel(const int64_t* __restrict__ cptr, const int* __re
   for (int64_t k = 0; b + k * G < n_chunks; ++k) {
     const int64_t pos = b + k * G;
     const int64_t c = list ? list[pos] : pos;
-    // stage of tile k: k % S, or for the row-pair feed (ng groups owning S / ng stages each)
-    // (k % ng) * (S / ng) + (k / ng) % (S / ng)  (kernels.cu pair_stage)
-    const int64_t sidx = ng > 1 ? (k % ng) * (S / ng) + (k / ng) % (S / ng) : k % S;
-    const int64_t stage = tl.pool_bytes + sidx * (int64_t)tl.stage_bytes;
+    const int64_t stage = tl.pool_bytes + (k % S) * (int64_t)tl.stage_bytes;
     uint4* r = rec + pos * kRecSlots;
     int* m = map + pos * kBcMapInts;
     bool ok = true;
@@ -344,21 +337,17 @@ __global__ void bc_plan_kernel(const int64_t* __restrict__ cptr, const int* __re
       }
     }
     m[0] = nneed;
-    int depth = 0;  // extra releases tile k waits for (row-pair feed only)
     for (int i = 0; i < nneed && ok; ++i) {
       int slot = -1;
       for (int p = 0; p < P; ++p)
         if (sblk[p] == need[i]) slot = p;
       if (slot < 0) {
-        for (int dd = depth; dd <= relax && slot < 0; ++dd) {
-          int64_t best = 1ll << 62;
-          for (int p = 0; p < P; ++p)
-            if (slast[p] <= k - S + dd && slast[p] < k && slast[p] < best) {
-              best = slast[p];
-              slot = p;
-            }
-          if (slot >= 0) depth = dd;
-        }
+        int64_t best = 1ll << 62;
+        for (int p = 0; p < P; ++p)
+          if (slast[p] <= k - S && slast[p] < best) {
+            best = slast[p];
+            slot = p;
+          }
         if (slot < 0) {
           ok = false;
           break;
@@ -394,10 +383,8 @@ __global__ void bc_plan_kernel(const int64_t* __restrict__ cptr, const int* __re
       cmd(3, s0 * 2, stage + tl.off_lcol, nslot * 2);
     }
     for (int q = n + 1; q < kRecSlots; ++q) r[q] = make_uint4(0u, 0u, 0u, 0u);
-    const uint32_t pz = pinfo ? (uint32_t)pinfo[c] : 0u;  // m | Ls << 8
-    r[0] = make_uint4((uint32_t)total, (uint32_t)(total - wbytes),
-                      (uint32_t)(nslot / kC) | (pinfo ? ((pz >> 8 & 0xFFu) << 16 | (pz & 0x1Fu) << 24) : 0u),
-                      (uint32_t)n | ((uint32_t)m[2] << 8) | ((uint32_t)depth << 24));
+    r[0] = make_uint4((uint32_t)total, (uint32_t)(total - wbytes), (uint32_t)(nslot / kC),
+                      (uint32_t)n | ((uint32_t)m[2] << 8));
     if (!ok) atomicOr(fail, 1);
   }
 }
@@ -435,9 +422,9 @@ int grid_for(int64_t n, int block) {
 cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* runs, const int* scol,
                             const int64_t* list, int64_t n_chunks, int grid, int R, bool with_w,
                             const TileLayout& tl, uint4* rec, int* map, uint16_t* lcol_bc, int* fail,
-                            const int* pinfo, int relax, int ng, cudaStream_t s) {
+                            cudaStream_t s) {
   bc_plan_kernel<<<(grid + 63) / 64, 64, 0, s>>>(cptr, nruns, runs, list, n_chunks, grid, R, with_w ? 1 : 0, tl, rec,
-                                                  map, fail, pinfo, relax, ng);
+                                                  map, fail);
   bc_lcol_kernel<<<grid_for(n_chunks * 32, 256), 256, 0, s>>>(scol, cptr, list, n_chunks, map, lcol_bc, fail);
   return cudaGetLastError();
 }

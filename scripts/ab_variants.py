@@ -1,6 +1,7 @@
 """A/B timing of sweep-kernel variants at full size (C3 by default), interleaved in rounds so
-that both see the same power-capped clock; y-line chunk order sized to each variant's grid.
-One JSON line per (round, R, variant): sweep ms, HBM roofline fraction, deviation of mu."""
+that all see the same power-capped clock; by default each runs in the chunk order the library
+picks for it.  One JSON line per (round, R, variant): sweep ms, HBM roofline fraction, deviation
+of mu from the round's first variant, SM clock and board power sampled after a warm call."""
 import argparse
 import json
 import os
@@ -30,7 +31,8 @@ def main():
     ap.add_argument("--M", type=int, default=2000)
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--names", default="", help="comma list of variant names (default: all of the width)")
-    ap.add_argument("--order", default="ylines", choices=["ylines", "none", "lib"])
+    ap.add_argument("--order", default="lib", choices=["ylines", "none", "lib", "ystrips"],
+                    help="lib: the library's own chunk order; ylines: workloads.chunk_order_ylines; none: storage")
     args = ap.parse_args()
     import torch
 
@@ -43,7 +45,6 @@ def main():
     a, b = scale_factors(*gershgorin(rp, col, val))
     n, nnz = lat.n, int(rp[-1])
     hbm = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6556.8
-    ctas = {"tiled.bc.lpr8.u4": 1, "tiled.bc.lpr4.u4.wr": None}
     for rnd in range(args.rounds):
         for R in (int(r) for r in args.R.split(",")):
             names = [kpm.variant_name(R, v) for v in range(32) if kpm.variant_name(R, v)]
@@ -57,8 +58,15 @@ def main():
                 with kpm.KpmContext() as ctx:
                     ctx.set_matrix(rp, col, val, a, b)
                     if args.order == "ylines" and ".bc." in name:
-                        per_sm = 1 if name.startswith("pair") or R == 32 else (2 if R == 16 else 3)
+                        per_sm = 1 if R == 32 else (2 if R == 16 else 3)
                         ctx.set_chunk_order(chunk_order_ylines(lat, sms * per_sm))
+                    elif args.order == "ystrips" and ".bc." in name:
+                        from workloads.ti_lattice import chunk_order_ystrips
+
+                        per_sm = 1 if R == 32 else (2 if R == 16 else 3)
+                        ctx.set_chunk_order(chunk_order_ystrips(lat, sms * per_sm))
+                    elif args.order == "none":
+                        ctx.set_chunk_order(np.arange(ctx.sell_info().n_chunks, dtype=np.int64))
                     ctx.moments(args.M, R, SEED, want_eta=False)
                     mhz, watt = clock()
                     mu, _ = ctx.moments(args.M, R, SEED, want_eta=False)
@@ -67,7 +75,7 @@ def main():
                 if ref is None:
                     ref = mu
                 bytes_ = 20 * nnz + 48 * R * n
-                row = dict(round=rnd, R=R, variant=name, ran=ran, sweep_ms=sw, frac=bytes_ / sw / 1e6 / hbm,
+                row = dict(round=rnd, R=R, variant=name, order=args.order, ran=ran, sweep_ms=sw, frac=bytes_ / sw / 1e6 / hbm,
                            gflops=R * (8 * nnz + 34 * n) / sw / 1e6, dmu=float(np.max(np.abs(mu - ref)) / ref[0]),
                            sm_mhz=mhz, power_w=watt, lattice=[nx, ny, nz], M=args.M, time=time.time())
                 print(json.dumps(row), flush=True)

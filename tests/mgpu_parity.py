@@ -77,9 +77,8 @@ def main():
             ctx.set_matrix(rp, col, val, a, b, n_global=n_g, row_begin=r0)
         # the rank's SELL copy and halo map, bit-exact against the numpy reference builder
         bounds_all = np.array(bounds if dims == "random" else [q * lat.rows_per_plane for q in planes], dtype=np.int64)
-        ref = sell_ref.pair_order(sell_ref.build_sell(rp_g[r0:r1 + 1] - rp_g[r0], col_g[rp_g[r0]:rp_g[r1]],
-                                                      val_g[rp_g[r0]:rp_g[r1]], row_begin=r0, row_end=r1,
-                                                      row_begins=bounds_all))
+        ref = sell_ref.build_sell(rp_g[r0:r1 + 1] - rp_g[r0], col_g[rp_g[r0]:rp_g[r1]], val_g[rp_g[r0]:rp_g[r1]],
+                                  row_begin=r0, row_end=r1, row_begins=bounds_all)
         ex = ctx.export_sell()
         sell_ok = all(np.array_equal(ex[k], ref[k]) for k in ("cptr", "col", "val", "perm", "halo"))
         sell_all = [None] * world

@@ -36,9 +36,8 @@ def problem(dims, potential=None, periodic_z=False):
 
 
 def ref_sell(rp, col, val, **kw):
-    """The product's SELL contract: the R18 layout of sell_ref.build_sell, then the row-pair
-    entry order (sell_ref.pair_order, R18b)."""
-    return sell_ref.pair_order(sell_ref.build_sell(rp, col, val, **kw))
+    """The product's SELL contract: the layout of the numpy reference builder (R18)."""
+    return sell_ref.build_sell(rp, col, val, **kw)
 
 
 def check(eta_g, mu_g, eta_o, cols=None):
@@ -86,11 +85,9 @@ def test_zero_potential_and_sigma(pkg, sigma):
         ctx.set_matrix(rp, col, val, a, b)
         mu, eta = ctx.moments(M, R, 77)
         s = ctx.export_sell()
-        s["pinfo"] = ctx.export_pairs()
     eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, 77)
     check(eta, mu, eta_o)
     ref = ref_sell(rp, col, val, C=32, sigma=sigma)
-    assert np.array_equal(s["pinfo"], ref["pinfo"])
     assert np.array_equal(s["cptr"], ref["cptr"])
     assert np.array_equal(s["col"], ref["col"])
     assert np.array_equal(s["val"], ref["val"])
@@ -102,12 +99,10 @@ def test_sell_bit_exact_c1(pkg):
     with pkg.KpmContext() as ctx:
         ctx.set_matrix(rp, col, val, a, b)
         s = ctx.export_sell()
-        s["pinfo"] = ctx.export_pairs()
     ref = ref_sell(rp, col, val)
-    for k in ("cptr", "col", "val", "perm", "pinfo"):
+    for k in ("cptr", "col", "val", "perm"):
         assert np.array_equal(s[k], ref[k]), k
     assert s["cptr"][-1] == 13 * lat.n
-    assert np.all(s["pinfo"] == (3 | 8 << 8))  # TI: orbitals {0,3}, {1,2} share 8 columns
 
 
 def test_exact_trace_bloch_v0(pkg):
@@ -275,11 +270,10 @@ def test_device_build(pkg, dims):
         with pkg.KpmContext() as ctx:
             ctx.set_matrix(rp_d, col_d, val_d, a, b, n_global=lat.n, mem=pkg.KPM_MEM_DEVICE)
             s = ctx.export_sell()
-            s["pinfo"] = ctx.export_pairs()
             mu, eta = ctx.moments(M, R, SEED)
-            assert ctx.last_kernel().startswith(("tiled", "pair"))
+            assert ctx.last_kernel().startswith("tiled")
         ref = ref_sell(rp, col, val)
-        for k in ("cptr", "col", "val", "perm", "pinfo"):
+        for k in ("cptr", "col", "val", "perm"):
             assert np.array_equal(s[k], ref[k]), k
         check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, M, R, SEED))
     torch.cuda.synchronize()
@@ -342,7 +336,7 @@ def test_rows_without_diagonal(pkg, R):
             else:
                 ctx.set_matrix(rp, col, val, a, b)
             mu, eta = ctx.moments(M, R, SEED)
-            assert ctx.last_kernel().startswith(("tiled", "pair"))
+            assert ctx.last_kernel().startswith("tiled")
             s = ctx.export_sell()
         check(eta, mu, eta_o)
         assert np.array_equal(s["col"], ref["col"]) and np.array_equal(s["val"], ref["val"])

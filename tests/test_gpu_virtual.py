@@ -6,159 +6,46 @@ stores boundary rows straight into the neighbours' halo slots -- plain device po
 instead of CUDA IPC mappings), the flag-epoch ordering (cuStreamWaitValue32 / WriteValue32), and
 the single eta reduction at the end (host all-gather in rank order here instead of
 ncclAllReduce).  Checked against the oracle on the global matrix (1e-10 gate), the SELL copy and
-halo plan bit for bit against the numpy references, and P-invariance."""
-import threading
+halo plan bit for bit against the numpy references, and P-invariance.  Each case runs in a
+subprocess (tests/vranks_parity.py) with CUDA_DEVICE_MAX_CONNECTIONS=32 and a hard timeout."""
+import json
+import os
+import subprocess
+import sys
 
-import numpy as np
 import pytest
 
-import oracle
-from oracle import sell_ref
-from workloads.ti_lattice import SEED, Lattice, gershgorin, generate_csr, scale_factors
-
 pytestmark = pytest.mark.gpu
-TOL = 1e-10
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.fixture(scope="module")
-def pkg():
+def run(*args, timeout=600):
     import torch
 
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
-    from paper_1410_5242_b200 import build
-
-    build.build()
-    import paper_1410_5242_b200 as p
-
-    return p
-
-
-def run_ranks(pkg, P, fn, timeout=600):
-    """fn(ctx, rank) on P virtual ranks in P threads; returns the per-rank results."""
-    group = pkg.VirtualGroup(P)
-    out, err = [None] * P, [None] * P
-
-    def worker(r):
-        try:
-            with pkg.KpmContext(device=0, nranks=P, rank=r, vgroup=group) as ctx:
-                out[r] = fn(ctx, r)
-        except BaseException as e:  # noqa: BLE001 -- reported below
-            err[r] = e
-
-    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(P)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join(timeout)
-    assert not any(t.is_alive() for t in th), "virtual ranks hung"
-    group.close()
-    for e in err:
-        if e is not None:
-            raise e
-    return out
-
-
-def ti_problem(dims):
-    lat = Lattice(*dims)
-    rp, col, val = generate_csr(lat)
-    return lat, rp, col, val
-
-
-def mixed_problem(P):
-    """TI lattice plus seeded random long-range Hermitian couplings among rank 1's rows: rank 1's
-    chunks read scattered rows (its tile / block-cache plans do not fit), the others stay
-    stencil-like, so the ranks must agree on a kernel variant every rank can run."""
-    lat, rp, col, val = ti_problem((4 * P, 5, 16))
-    n = lat.n
-    r0, r1 = n // P, 2 * n // P
-    rng = np.random.default_rng(41)
-    i = rng.integers(r0, r1, 600)
-    j = rng.integers(r0, r1, 600)
-    z = 0.05 * (rng.normal(size=600) + 1j * rng.normal(size=600))
-    import scipy.sparse as sp
-
-    h = sp.csr_matrix((val, col, rp), shape=(n, n)) + sp.coo_matrix((z, (i, j)), shape=(n, n)).tocsr()
-    h = (h + sp.coo_matrix((np.conj(z), (j, i)), shape=(n, n)).tocsr()).tocsr()
-    h.sort_indices()
-    return n, h.indptr.astype(np.int64), h.indices.astype(np.int64), h.data.astype(np.complex128)
-
-
-def check(mu_g, eta_g, eta_o):
-    mu_o, _ = oracle.eta_to_mu(eta_o)
-    assert np.max(np.abs(eta_g - eta_o) / eta_o[:, :1].real) <= TOL
-    assert np.max(np.abs(mu_g - mu_o)) / mu_o[0] <= TOL
-
-
-def run_case(pkg, P, n, rp, col, val, bounds, M, R, seed, want_v0=False):
-    a, b = scale_factors(*gershgorin(rp, col, val))
-    rng = np.random.default_rng(5)
-    v0 = rng.normal(size=(n, 2)) + 1j * rng.normal(size=(n, 2))
-
-    def fn(ctx, r):
-        r0, r1 = bounds[r], bounds[r + 1]
-        lrp = rp[r0:r1 + 1] - rp[r0]
-        lcol, lval = col[rp[r0]:rp[r1]], val[rp[r0]:rp[r1]]
-        ctx.set_matrix(lrp, lcol, lval, a, b, n_global=n, row_begin=r0)
-        mu, eta = ctx.moments(M, R, seed)
-        res = dict(mu=mu, eta=eta, kernel=ctx.last_kernel(), sell=ctx.export_sell(), pairs=ctx.export_pairs(),
-                   halo=ctx.export_halo(), lrp=lrp, lcol=lcol, lval=lval)
-        if want_v0:
-            res["v0"] = ctx.moments_v0(M, v0[r0:r1])
-        return res
-
-    out = run_ranks(pkg, P, fn)
-    eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, seed)
-    for r, o in enumerate(out):
-        check(o["mu"], o["eta"], eta_o)
-        assert np.array_equal(o["mu"], out[0]["mu"])  # identical on every rank (one reduction)
-        assert o["kernel"] == out[0]["kernel"]          # every rank ran the same variant
-        r0, r1 = bounds[r], bounds[r + 1]
-        ref = sell_ref.pair_order(sell_ref.build_sell(o["lrp"], o["lcol"], o["lval"], row_begin=r0, row_end=r1,
-                                                      row_begins=np.asarray(bounds)))
-        for k in ("cptr", "col", "val", "perm", "halo"):
-            assert np.array_equal(o["sell"][k], ref[k]), (r, k)
-        assert np.array_equal(o["pairs"], ref["pinfo"])
-        recv = pkg.plan_recv(np.asarray(bounds), r, o["lrp"], o["lcol"])
-        assert np.array_equal(o["halo"][0], recv)  # kpm_export_halo == the host planner
-    if want_v0:
-        eta_vo = oracle.kpm_eta_v0(rp, col, val, a, b, M, v0)
-        for o in out:
-            mu_v, eta_v = o["v0"]
-            assert np.max(np.abs(eta_v - eta_vo) / eta_vo[:, :1].real) <= TOL
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "vranks_parity.py"), *map(str, args)],
+                         capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=env)
+    lines = [l for l in res.stdout.splitlines() if l.startswith("VRANKS_RESULT ")]
+    assert res.returncode == 0 and lines, res.stdout[-3000:] + res.stderr[-3000:]
+    out = json.loads(lines[-1][len("VRANKS_RESULT "):])
+    assert out["ok"], out
     return out
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
 @pytest.mark.parametrize("R", [32, 8])
-def test_virtual_ranks_ti_slabs(pkg, P, R):
-    """x-slabs of a TI lattice (2 planes per rank at P = 8): the default kernels (block-cache feed
-    at R = 32) with the fused exchange and the library's chunk order on every rank."""
-    lat, rp, col, val = ti_problem((2 * P, 6, 16))
-    planes = [lat.nx * q // P for q in range(P + 1)]
-    bounds = [q * lat.rows_per_plane for q in planes]
-    out = run_case(pkg, P, lat.n, rp, col, val, bounds, 64, R, SEED + P, want_v0=(R == 8))
-    with pkg.KpmContext() as c1:  # P-invariance against one rank
-        a, b = scale_factors(*gershgorin(rp, col, val))
-        c1.set_matrix(rp, col, val, a, b)
-        mu1, _ = c1.moments(64, R, SEED + P)
-    assert np.max(np.abs(out[0]["mu"] - mu1)) / mu1[0] <= TOL
+def test_virtual_ranks_ti_slabs(P, R):
+    out = run("ti", P, R)
+    if R == 32:
+        assert out["kernel"].startswith("tiled.bc")  # the block-cache feed, one plan per list
 
 
 @pytest.mark.parametrize("P", [2, 4])
-def test_virtual_ranks_uneven_irregular(pkg, P):
-    """Uneven row split of a TI lattice with random long-range couplings on rank 1: halo runs are
-    scattered, some ranks cannot run the tiled / block-cache feeds -- all ranks agree on one
-    variant (no hang), results oracle-exact."""
-    n, rp, col, val = mixed_problem(P)
-    w = np.arange(1, P + 1, dtype=float)
-    bounds = [0] + [int(x) for x in np.round(np.cumsum(w) / w.sum() * n)]
-    bounds[-1] = n
-    run_case(pkg, P, n, rp, col, val, bounds, 48, 32, 23)
+def test_virtual_ranks_uneven_irregular(P):
+    run("uneven", P)
 
 
-def test_virtual_group_rejects_mismatch(pkg):
-    g = pkg.VirtualGroup(3)
-    with pytest.raises(pkg.KpmError):
-        pkg.KpmContext(device=0, nranks=2, rank=0, vgroup=g)
-    g.close()
+def test_virtual_group_rejects_mismatch():
+    assert run("mismatch")["rejected"]
