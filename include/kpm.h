@@ -249,11 +249,12 @@ kpm_status kpm_plan_send(int64_t row_begin, int64_t row_end, int peer, int64_t n
 /* Host-only: the library's default chunk order (the locality walk kpm_moments uses when no
  * kpm_set_chunk_order is given; DESIGN.md §7 "Chunk order").  nbr_ptr (n_chunks+1) / nbr: for
  * every chunk the chunks all of whose C rows it reads (block neighbours, CSR layout, ids in
- * [0, n_chunks)); grid: CTAs of the sweep launch (lines per round); skip (NULL or n_chunks
- * flags): chunks left out of the lines and put last (the edge chunks of a multi-rank split).
- * order: out, n_chunks int64, a permutation.  KPM_ERANGE for a neighbour id out of range. */
+ * [0, n_chunks)); grid: CTAs of the sweep launch (lines per round); width: 1 = single lines, 2 =
+ * strips of two adjacent lines walked step by step; skip (NULL or n_chunks flags): chunks left out
+ * of the lines and put last (the edge chunks of a multi-rank split).  order: out, n_chunks int64,
+ * a permutation.  KPM_ERANGE for a neighbour id out of range. */
 kpm_status kpm_plan_chunk_order(int64_t n_chunks, const int64_t* nbr_ptr, const int64_t* nbr, int64_t grid,
-                                const int8_t* skip, int64_t* order);
+                                int width, const int8_t* skip, int64_t* order);
 
 /* Density of states from the moments (north_star item 5; Eq. (2) `DOS`; the
  * "second computationally inexpensive step" of P:258-260).  Host only, no context.

@@ -88,7 +88,7 @@ def load_library():
     lib.kpm_dos.argtypes = [i32, P, dbl, dbl, i32, P, i32, P, P]
     lib.kpm_plan_recv.argtypes = [i32, P, i32, P, P, P, P]
     lib.kpm_plan_send.argtypes = [i64, i64, i32, i64, P, P, P]
-    lib.kpm_plan_chunk_order.argtypes = [i64, P, P, i64, P, P]
+    lib.kpm_plan_chunk_order.argtypes = [i64, P, P, i64, i32, P, P]
     lib.kpm_destroy.argtypes = [P]
     lib.kpm_destroy.restype = None
     for name in ABI_SYMBOLS:
@@ -171,7 +171,7 @@ def plan_send(row_begin, row_end, peer, req):
     return out[: n.value]
 
 
-def plan_chunk_order(nbr_ptr, nbr, grid, skip=None):
+def plan_chunk_order(nbr_ptr, nbr, grid, skip=None, width=1):
     """kpm_plan_chunk_order: the library's default chunk order from block-neighbour lists."""
     lib = load_library()
     nbr_ptr = np.ascontiguousarray(nbr_ptr, dtype=np.int64)
@@ -179,7 +179,8 @@ def plan_chunk_order(nbr_ptr, nbr, grid, skip=None):
     n = len(nbr_ptr) - 1
     sk = None if skip is None else np.ascontiguousarray(skip, dtype=np.int8)
     out = np.zeros(max(n, 1), dtype=np.int64)
-    st = lib.kpm_plan_chunk_order(n, _ptr(nbr_ptr), _ptr(nbr) if len(nbr) else None, int(grid), _ptr(sk), _ptr(out))
+    st = lib.kpm_plan_chunk_order(n, _ptr(nbr_ptr), _ptr(nbr) if len(nbr) else None, int(grid), int(width), _ptr(sk),
+                                  _ptr(out))
     if st != KPM_OK:
         raise KpmError(st, "kpm_plan_chunk_order")
     return out[:n]

@@ -14,9 +14,15 @@
 // memory) and the other neighbours are the current tiles of other CTAs (L2 hits).  Lines left
 // over after the last full round, and chunks in no line, follow in storage order.  Chunks with
 // skip[c] != 0 (the edge chunks of a multi-rank split) are kept out of the lines and go last.
+// width = 2 walks strips of two adjacent lines step by step (c, c', c + d, c' + d, ... with c' =
+// c + d2, d2 the next frequent offset: TI x): a tile's neighbour on the strip's inside is then a
+// block its CTA already holds.  Measured on C3: -2 % sweep time for the R = 32 block-cache
+// kernel (1 CTA per SM, 10-block pool), +2 % for the R = 16 ones (2 CTAs per SM), so the kernel
+// table chooses the width per variant.
 #include <stdint.h>
 
 #include <algorithm>
+#include <array>
 #include <map>
 #include <vector>
 
@@ -39,7 +45,7 @@ void block_neighbours(int64_t n_chunks, const int* nruns, const int* runs, int m
 }
 
 std::vector<int64_t> line_order(int64_t n_chunks, const std::vector<int64_t>& ptr, const std::vector<int64_t>& nbr,
-                                int64_t G, const std::vector<char>& skip) {
+                                int64_t G, const std::vector<char>& skip, int width) {
   auto in = [&](int64_t c) { return c >= 0 && c < n_chunks && (skip.empty() || !skip[c]); };
   auto is_nbr = [&](int64_t c, int64_t b) {
     for (int64_t i = ptr[c]; i < ptr[c + 1]; ++i)
@@ -55,11 +61,13 @@ std::vector<int64_t> line_order(int64_t n_chunks, const std::vector<int64_t>& pt
     for (int64_t i = ptr[c]; i < ptr[c + 1]; ++i)
       if (nbr[i] > c && in(nbr[i])) ++freq[nbr[i] - c];
   }
-  int64_t d = 0;
+  int64_t d = 0, d2 = 0;  // line direction; the next frequent offset (strips of width 2)
   for (const auto& kv : freq)
     if (2 * kv.second >= n_in) {
-      d = kv.first;
-      break;
+      if (!d)
+        d = kv.first;
+      else if (!d2)
+        d2 = kv.first;
     }
   std::vector<int64_t> order;
   order.reserve(n_chunks);
@@ -73,20 +81,45 @@ std::vector<int64_t> line_order(int64_t n_chunks, const std::vector<int64_t>& pt
       for (int64_t x = c; linked(x); x += d) ++len;
       lines.push_back({c, len});
     }
-    // rounds of G lines of equal length (longest first, starts ascending inside a length)
-    std::stable_sort(lines.begin(), lines.end(), [](const auto& a, const auto& b) { return a.second > b.second; });
+    // width 2: pair each line (ascending start) with the unpaired equal-length line d2 further on
+    // whose chunks are block neighbours of its own; a unit = a line or a pair of lines
+    std::vector<std::array<int64_t, 3>> units;  // (start, length, partner start or -1)
+    if (width == 2 && d2 > 0) {
+      std::map<int64_t, size_t> at;
+      for (size_t l = 0; l < lines.size(); ++l) at[lines[l].first] = l;
+      std::vector<char> paired(lines.size(), 0);
+      for (size_t l = 0; l < lines.size(); ++l) {
+        if (paired[l]) continue;
+        const auto it = at.find(lines[l].first + d2);
+        if (it != at.end() && !paired[it->second] && lines[it->second].second == lines[l].second) {
+          bool adj = true;
+          for (int64_t k = 0; k < lines[l].second && adj; ++k)
+            adj = is_nbr(lines[l].first + k * d, lines[l].first + k * d + d2);
+          if (adj) {
+            paired[l] = paired[it->second] = 1;
+            units.push_back({lines[l].first, lines[l].second, lines[it->second].first});
+          }
+        }
+      }
+    } else {
+      for (const auto& ln : lines) units.push_back({ln.first, ln.second, -1});
+    }
+    // rounds of G units of equal length and kind (longest first, starts ascending inside a
+    // length), all CTAs at the same step; a pair advances both of its lines per step
+    std::stable_sort(units.begin(), units.end(), [](const auto& a, const auto& b) { return a[1] > b[1]; });
     size_t i = 0;
-    while (i < lines.size()) {
+    while (i < units.size()) {
       size_t j = i;
-      while (j < lines.size() && lines[j].second == lines[i].second) ++j;
+      while (j < units.size() && units[j][1] == units[i][1]) ++j;
       const size_t full = (j - i) / (size_t)G * (size_t)G;
       for (size_t r = i; r < i + full; r += (size_t)G)
-        for (int64_t step = 0; step < lines[i].second; ++step)
-          for (size_t l = r; l < r + (size_t)G; ++l) {
-            const int64_t c = lines[l].first + step * d;
-            order.push_back(c);
-            used[c] = 1;
-          }
+        for (int64_t step = 0; step < units[i][1]; ++step)
+          for (int lane = 0; lane < (units[i][2] >= 0 ? 2 : 1); ++lane)
+            for (size_t l = r; l < r + (size_t)G; ++l) {
+              const int64_t c = (lane ? units[l][2] : units[l][0]) + step * d;
+              order.push_back(c);
+              used[c] = 1;
+            }
       i = j;
     }
   }

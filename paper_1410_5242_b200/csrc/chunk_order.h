@@ -12,10 +12,11 @@ namespace kpm {
 void block_neighbours(int64_t n_chunks, const int* nruns, const int* runs, int max_runs, int C,
                       std::vector<int64_t>& ptr, std::vector<int64_t>& nbr);
 
-// Line walk in rounds of G lines (see chunk_order.cpp); skip (empty or n_chunks flags): chunks
-// kept out of the lines and appended last.  Returns a permutation of 0..n_chunks-1.
+// Line walk in rounds of G lines (width 1) or strips of two lines (width 2) (see chunk_order.cpp);
+// skip (empty or n_chunks flags): chunks kept out of the lines and appended last.  Returns a
+// permutation of 0..n_chunks-1.
 std::vector<int64_t> line_order(int64_t n_chunks, const std::vector<int64_t>& ptr, const std::vector<int64_t>& nbr,
-                                int64_t G, const std::vector<char>& skip);
+                                int64_t G, const std::vector<char>& skip, int width = 1);
 
 // 90th percentile over the chunks of the largest |b - c| to a block neighbour: the reuse distance
 // (in chunks) of a storage-order sweep, periodic wraps aside.

@@ -707,15 +707,23 @@ struct Variant {
     }
     return cudaGetLastError();
   }
+  // Also loads both the init and the main kernel (CUDA 12 loads modules lazily, and a load can
+  // synchronize the device: it must not happen inside the sweep loop, where another rank's stream
+  // of the same process may wait on a flag this thread has yet to enqueue -- virtual ranks).
   static int occupancy(int dyn_smem) {
     int n = 0;
+    cudaFuncAttributes fa;
     if constexpr (FEED == kStaged) {
+      cudaFuncGetAttributes(&fa, aug_spmmv_staged<R, LPR, U, true>);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_staged<R, LPR, U, false>, kThreads, kStagedSmem);
     } else if constexpr (FEED == kTiled) {
+      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB, BC>;
       auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB, BC>;
+      cudaFuncSetAttribute(k_init, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
       cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_main, tiled_threads<LPR, CS>(), dyn_smem);
     } else {
+      cudaFuncGetAttributes(&fa, aug_spmmv_direct<R, LPR, U, true>);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_direct<R, LPR, U, false>, kThreads, 0);
     }
     return n;
@@ -733,6 +741,7 @@ struct Entry {
   OccFn occ;
   int stages = 0;  // tiled feed: preferred ring depth (0 = plan_tiles default)
   int bc_ctas = 0;  // block-cache feed: CTAs per SM its shared-memory plan is sized for (0: not BC)
+  int strip = 1;    // chunk-order width the library's line walk uses for it (chunk_order.cpp)
 };
 #define KPM_VARIANT(R, LPR, U, F, NAME) {R, NAME, F, true, Variant<R, LPR, U, F>::launch, Variant<R, LPR, U, F>::occupancy}
 #define KPM_VARIANT_CS(R, LPR, U, CS, NAME) \
@@ -771,11 +780,13 @@ const Entry kTable[] = {
     KPM_VARIANT(8, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(8, 8, 4, kDirect, "direct.lpr8.u4"),
+    // R = 16: 8 lanes per row, 2 block columns per lane, 2 CTAs per SM (18 warps): -7.5 % vs the
+    // 4-lane map under the power cap (profiles/r02_variants/)
+    {16, "tiled.bc.lpr8.u4.wr", kTiled, false, Variant<16, 8, 4, kTiled, 1, false, 2, true>::launch,
+     Variant<16, 8, 4, kTiled, 1, false, 2, true>::occupancy, 2, 2},
     {16, "tiled.bc.lpr4.u4.wr", kTiled, false, Variant<16, 4, 4, kTiled, 1, false, 2, true>::launch,
      Variant<16, 4, 4, kTiled, 1, false, 2, true>::occupancy, 2, 2},
     KPM_VARIANT_WR_S(16, 4, 4, 2, "tiled.lpr4.u4.wr.s2"),
-    {16, "tiled.bc.lpr8.u4.wr", kTiled, false, Variant<16, 8, 4, kTiled, 1, false, 2, true>::launch,
-     Variant<16, 8, 4, kTiled, 1, false, 2, true>::occupancy, 2, 2},
     KPM_VARIANT(16, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT(16, 4, 2, kTiled, "tiled.lpr4.u2"),
     KPM_VARIANT_WR(16, 8, 4, "tiled.lpr8.u4.wr"),
@@ -784,8 +795,9 @@ const Entry kTable[] = {
     KPM_VARIANT_CS(16, 8, 4, 2, "tiled.lpr8.u4.cs2"),
     KPM_VARIANT(16, 8, 4, kStaged, "staged.lpr8.u4"),
     KPM_VARIANT(16, 8, 4, kDirect, "direct.lpr8.u4"),
+    // R = 32: walked in strips of two lines (-2 % under the power cap, profiles/r02_variants/)
     {32, "tiled.bc.lpr8.u4", kTiled, true, Variant<32, 8, 4, kTiled, 1, true, 1, true>::launch,
-     Variant<32, 8, 4, kTiled, 1, true, 1, true>::occupancy, 2, 1},
+     Variant<32, 8, 4, kTiled, 1, true, 1, true>::occupancy, 2, 1, 2},
     KPM_VARIANT(32, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT_WR(32, 8, 4, "tiled.lpr8.u4.wr"),
     KPM_VARIANT_CS(32, 8, 4, 2, "tiled.lpr8.u4.cs2"),
@@ -837,6 +849,11 @@ int base_variant(int R) {
       ++i;
     }
   return 0;
+}
+
+int variant_strip(int R, int variant) {
+  const Entry* e = find(R, variant);
+  return e ? e->strip : 1;
 }
 
 int variant_bc(int R, int variant) {
@@ -943,6 +960,14 @@ cudaError_t launch_sweep_kind(int R, int kind, const SweepArgs& a, int grid, cud
   for (const KindEntry& e : kKinds)
     if (e.R == R) return kind == kAugNoDot ? e.nodot(a, grid, s) : kind == kSpmmv ? e.spmmv(a, grid, s) : cudaErrorInvalidValue;
   return cudaErrorInvalidValue;
+}
+
+cudaError_t preload_aux_kernels() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, z4_init_kernel);
+  cudaFuncGetAttributes(&fa, v0_permute_kernel);
+  cudaFuncGetAttributes(&fa, eta_finalize_kernel);
+  return cudaGetLastError();
 }
 
 static int elementwise_grid(int64_t n_el) {

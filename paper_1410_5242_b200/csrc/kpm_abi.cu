@@ -33,6 +33,22 @@ using namespace kpm;
 // through this host rendezvous instead of NCCL, and whose fused halo exchange stores into the
 // other contexts' buffers through plain device pointers instead of CUDA IPC mappings.  The sweep
 // kernels, the edge / interior split and the flag-epoch protocol are the multi-GPU ones.
+// KPM_TRACE=1 (read once): progress lines on stderr (rank, step) -- hang diagnosis for the
+// multi-rank protocol.
+static bool trace_on() {
+  static const bool on = getenv("KPM_TRACE") && atoi(getenv("KPM_TRACE")) > 0;
+  return on;
+}
+#define KPM_TRACE_LINE(rank, ...)                 \
+  do {                                            \
+    if (trace_on()) {                             \
+      fprintf(stderr, "[kpm r%d] ", (int)(rank)); \
+      fprintf(stderr, __VA_ARGS__);               \
+      fprintf(stderr, "\n");                      \
+      fflush(stderr);                             \
+    }                                             \
+  } while (0)
+
 struct kpm_vgroup {
   int P = 0;
   std::mutex mu;
@@ -43,6 +59,7 @@ struct kpm_vgroup {
   // all-gather of variable-length int64 vectors; every rank gets every rank's vector
   std::vector<std::vector<int64_t>> allgatherv(int rank, const std::vector<int64_t>& mine) {
     std::unique_lock<std::mutex> lk(mu);
+    KPM_TRACE_LINE(rank, "vgroup rendezvous %lld (%zu words)", (long long)gen, mine.size());
     slot[rank] = mine;
     const int64_t g = gen;
     if (++arrived == P) {
@@ -115,9 +132,9 @@ struct kpm_ctx {
   std::vector<int64_t> order_h;     // chunk processing order given by kpm_set_chunk_order
   bool order_user = false;          // order_h is in force (else the library's own choice)
   int64_t* order_list = nullptr;    // device copy of the installed order for single-rank sweeps
-  int64_t order_id = -3;            // installed order: -1 user, 0 storage, G > 0 line walk for grid G
+  int64_t order_id = -3;            // installed order: -1 user, 0 storage, 4 G + w: line walk of width w, grid G
   int64_t order_gen = 0;            // bumped by every install (keys of the block-cache plan, CUDA graph)
-  std::map<int64_t, std::vector<int64_t>> auto_order;  // line walk per grid (chunk_order.cpp)
+  std::map<int64_t, std::vector<int64_t>> auto_order;  // line walk per (grid, width) (chunk_order.cpp)
   int adj_state = 0;                // block-neighbour lists: 0 not built, 1 built, -1 unavailable
   std::vector<int64_t> adj_ptr, adj;
   int64_t adj_maxoff = 0;          // typical_block_offset of the matrix (chunks)
@@ -265,6 +282,11 @@ extern "C" kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt) {
       kpm_destroy(ctx);
       return r != ncclSuccess ? KPM_ENCCL : KPM_ECUDA;
     }
+  }
+  if (opt->nranks > 1 && (e = preload_aux_kernels()) != cudaSuccess) {  // before any flag wait can exist
+    g_create_err = std::string("CUDA: ") + cudaGetErrorString(e);
+    kpm_destroy(ctx);
+    return KPM_ECUDA;
   }
   ctx->variant_override = env_int("KPM_VARIANT", -1);
   ctx->grid_per_sm = std::max(0, env_int("KPM_GRID_PER_SM", 0));
@@ -535,7 +557,7 @@ static kpm_status ensure_adjacency(kpm_ctx* ctx) {
 // The chunk order a launch of `grid` CTAs runs: the caller's (kpm_set_chunk_order), else the
 // line walk when want_lines (block-cache kernels; any kernel whose storage-order neighbour
 // window exceeds 32 MB), else storage order.
-static kpm_status ensure_order(kpm_ctx* ctx, int64_t grid, bool bc_kernel, int Rk) {
+static kpm_status ensure_order(kpm_ctx* ctx, int64_t grid, bool bc_kernel, int Rk, int width) {
   if (ctx->order_user) return install_order(ctx, ctx->order_h, -1);
   kpm_status st = ensure_adjacency(ctx);
   if (st != KPM_OK) return st;
@@ -543,13 +565,14 @@ static kpm_status ensure_order(kpm_ctx* ctx, int64_t grid, bool bc_kernel, int R
   // of the reuse distance (TI: two x-planes; C4 at R = 32: 65.5 MB, C3: 16.4 MB)
   const bool big_window = ctx->adj_state == 1 && 2.0 * (double)ctx->adj_maxoff * kC * Rk * 16.0 > 32e6;
   if (ctx->adj_state == 1 && (bc_kernel || big_window) && env_int("KPM_AUTO_ORDER", 1)) {
-    std::vector<int64_t>& o = ctx->auto_order[grid];
+    const int64_t id = grid * 4 + width;
+    std::vector<int64_t>& o = ctx->auto_order[id];
     if (o.empty()) {
       std::vector<char> skip;
       if (ctx->opt.nranks > 1) skip = ctx->edge_flag;
-      o = line_order(ctx->sell.n_chunks, ctx->adj_ptr, ctx->adj, grid, skip);
+      o = line_order(ctx->sell.n_chunks, ctx->adj_ptr, ctx->adj, grid, skip, width);
     }
-    return install_order(ctx, o, grid);
+    return install_order(ctx, o, id);
   }
   return install_order(ctx, {}, 0);
 }
@@ -1082,9 +1105,10 @@ static kpm_status select_variant(kpm_ctx* ctx, int Rk, int& variant, TileLayout&
     int g = 1;
     if (ok) {
       const int dyn = variant_tiled(Rk, v) ? pl.pool_bytes + pl.stages * pl.stage_bytes : 0;
-      const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, sweep_occupancy(Rk, v, dyn));
+      const int occ_q = sweep_occupancy(Rk, v, dyn);  // also loads the variant's kernels (kernels.cu)
+      const int occ = ctx->grid_per_sm ? ctx->grid_per_sm : std::max(1, occ_q);
       g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * occ, s.n_chunks));
-      if ((st = ensure_order(ctx, g, bcc > 0, Rk)) != KPM_OK) return st;
+      if ((st = ensure_order(ctx, g, bcc > 0, Rk, variant_strip(Rk, v))) != KPM_OK) return st;
       if (bcc && (st = build_bc_plan(ctx, Rk, v, pl, g, ok)) != KPM_OK) return st;
     }
     if (ctx->opt.nranks > 1 && !cached) {  // agree, so that every rank runs the same launches
@@ -1095,7 +1119,7 @@ static kpm_status select_variant(kpm_ctx* ctx, int Rk, int& variant, TileLayout&
     if (ok) {
       // re-install the chosen kernel's order (a plan tried after it may have replaced it; both
       // calls are no-ops when nothing changed)
-      if ((st = ensure_order(ctx, g, bcc > 0, Rk)) != KPM_OK) return st;
+      if ((st = ensure_order(ctx, g, bcc > 0, Rk, variant_strip(Rk, v))) != KPM_OK) return st;
       if (bcc && (st = build_bc_plan(ctx, Rk, v, pl, g, ok)) != KPM_OK) return st;
       if (!ok) return fail(ctx, KPM_ESTATE, "internal: block-cache plan changed");
       variant = v;
@@ -1154,6 +1178,8 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   TileLayout tl;
   bool bc = false;
   if ((st = select_variant(ctx, Rk, variant, tl, grid, bc)) != KPM_OK) return st;
+  KPM_TRACE_LINE(ctx->opt.rank, "variant selected: %s (fused %d, edge %lld, interior %lld)", variant_name(Rk, variant),
+                 (int)ctx->fused, (long long)ctx->n_edge, (long long)ctx->n_interior);
   const int rec_index = 2 * __builtin_ctz(Rk) + (variant_wstage(Rk, variant) ? 1 : 0);
   ctx->last_variant = variant_name(Rk, variant);
   const bool multi = ctx->opt.nranks > 1;
@@ -1228,12 +1254,19 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     sa.partials = part;
     if (bc) sa.rec = ctx->bc_rec;
     if (ctx->fused) {
+      // Virtual ranks: every rank has enqueued its flag write for this epoch before any rank
+      // enqueues a wait for it, so no stream ever waits on work its host thread has yet to
+      // enqueue -- an implicit device synchronisation by one thread (e.g. a lazy module load in
+      // a launch) would otherwise wait for a stream that waits for that very thread.
+      if (ctx->vg && m > 0) ctx->vg->allgatherv(ctx->opt.rank, {});
       // V's halo slots were written by the neighbours' previous edge launch: wait for their flags
       if (m > 0)
         for (int q : ctx->src_peers)
           if (g_wait_value32(str, (CUdeviceptr)(ctx->flags + q), ctx->epoch, CU_STREAM_WAIT_VALUE_GEQ) !=
               CUDA_SUCCESS)
             return fail(ctx, KPM_ECUDA, "cuStreamWaitValue32 failed");
+      KPM_TRACE_LINE(ctx->opt.rank, "sweep %d: waits on %zu peers for epoch %u enqueued", m,
+                     m > 0 ? ctx->src_peers.size() : (size_t)0, ctx->epoch);
       const bool send = m + 1 < n_sweeps;
       sa.n_peer = send ? (int)ctx->send_runs.size() : 0;
       for (int i = 0; i < sa.n_peer; ++i)
@@ -1279,6 +1312,8 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     }
     KPM_CUDA(cudaEventRecord(ctx->sweep_ev[0], str));
   }
+  KPM_TRACE_LINE(ctx->opt.rank, "run_block: start block enqueued, %d sweeps, variant %s, grid %d", n_sweeps,
+                 ctx->last_variant.c_str(), grid);
   // a2: init sweep, eta_0, eta_1
   if ((st = sweep(0)) != KPM_OK) return st;
   if (timing) KPM_CUDA(cudaEventRecord(ctx->sweep_ev[1], str));
@@ -1318,14 +1353,19 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
     for (int m = 1; m < n_sweeps; ++m) {
       if ((st = sweep(m)) != KPM_OK) return st;
       if (timing) KPM_CUDA(cudaEventRecord(ctx->sweep_ev[m + 1], str));
+      KPM_TRACE_LINE(ctx->opt.rank, "sweep %d enqueued (epoch %u)", m, ctx->epoch);
     }
   }
+  KPM_TRACE_LINE(ctx->opt.rank, "all sweeps enqueued");
   KPM_CUDA(cudaEventRecord(ctx->ev[2], str));
   // a4: deterministic grid reduction of all sweeps' partials
   KPM_CUDA(launch_eta_finalize(ctx->partials, n_sweeps, Rk, grid * parts, ctx->eta_even, ctx->eta_odd, str));
   if (multi && ctx->vg) {  // virtual ranks: host all-gather, sum in rank order, back to the device
     const size_t ne = (size_t)n_sweeps * Rk * 2;
     std::vector<int64_t> mine(2 * ne);
+    KPM_TRACE_LINE(ctx->opt.rank, "eta reduction: waiting for the stream");
+    KPM_CUDA(cudaStreamSynchronize(str));
+    KPM_TRACE_LINE(ctx->opt.rank, "eta reduction: stream done");
     KPM_CUDA(cudaMemcpyAsync(mine.data(), ctx->eta_even, sizeof(double) * ne, cudaMemcpyDeviceToHost, str));
     KPM_CUDA(cudaMemcpyAsync(mine.data() + ne, ctx->eta_odd, sizeof(double) * ne, cudaMemcpyDeviceToHost, str));
     KPM_CUDA(cudaStreamSynchronize(str));

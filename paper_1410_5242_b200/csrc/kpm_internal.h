@@ -121,6 +121,8 @@ cudaError_t launch_aug_spmmv(int R, int variant, bool init, const SweepArgs& a, 
 int check_hermitian(const int64_t* rp, const int64_t* col, const double* val, int64_t n_loc, int64_t row_begin,
                     int64_t row_end, int64_t n_global, double rtol, std::string& msg);  // hermitian.cpp
 cudaError_t launch_sweep_kind(int R, int kind, const SweepArgs& a, int grid, cudaStream_t s);
+// Load the start-block and eta kernels now (lazy module loading may synchronize the device).
+cudaError_t preload_aux_kernels();
 // eta[m][r] (double2) for m in [0, n_sweeps) from partials[m][3R][width] (width = launches x grid)
 cudaError_t launch_eta_finalize(const double* partials, int n_sweeps, int R, int width, double2* eta_even,
                                 double2* eta_odd, cudaStream_t s);
@@ -167,6 +169,7 @@ cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* ru
 TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas);
 int variant_bc(int R, int variant);  // block-cache feed: CTAs per SM it is planned for, 0 = other feed
 int base_variant(int R);             // first variant of width R that is not a block-cache feed
+int variant_strip(int R, int variant);  // width (1, 2) of the library's line walk for this variant
 cudaError_t launch_build_records(const int64_t* cptr, const int* nruns, const int* runs, int64_t n_chunks, int R,
                                  int off_w, int off_val, int off_lcol, uint4* rec, cudaStream_t s);
 

@@ -59,8 +59,9 @@ extern "C" kpm_status kpm_plan_send(int64_t row_begin, int64_t row_end, int peer
 }
 
 extern "C" kpm_status kpm_plan_chunk_order(int64_t n_chunks, const int64_t* nbr_ptr, const int64_t* nbr, int64_t grid,
-                                           const int8_t* skip, int64_t* order) {
-  if (n_chunks < 0 || !nbr_ptr || (nbr_ptr[n_chunks] > 0 && !nbr) || grid < 1 || !order) return KPM_EINVAL;
+                                           int width, const int8_t* skip, int64_t* order) {
+  if (n_chunks < 0 || !nbr_ptr || (nbr_ptr[n_chunks] > 0 && !nbr) || grid < 1 || !order || width < 1 || width > 2)
+    return KPM_EINVAL;
   std::vector<int64_t> ptr(nbr_ptr, nbr_ptr + n_chunks + 1), nb(nbr, nbr + nbr_ptr[n_chunks]);
   for (int64_t c = 0; c < n_chunks; ++c)
     if (ptr[c + 1] < ptr[c]) return KPM_EINVAL;
@@ -68,7 +69,7 @@ extern "C" kpm_status kpm_plan_chunk_order(int64_t n_chunks, const int64_t* nbr_
     if (b < 0 || b >= n_chunks) return KPM_ERANGE;
   std::vector<char> sk;
   if (skip) sk.assign(skip, skip + n_chunks);
-  const std::vector<int64_t> o = line_order(n_chunks, ptr, nb, grid, sk);
+  const std::vector<int64_t> o = line_order(n_chunks, ptr, nb, grid, sk, width);
   std::copy(o.begin(), o.end(), order);
   return KPM_OK;
 }

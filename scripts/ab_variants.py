@@ -31,7 +31,7 @@ def main():
     ap.add_argument("--M", type=int, default=2000)
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--names", default="", help="comma list of variant names (default: all of the width)")
-    ap.add_argument("--order", default="lib", choices=["ylines", "none", "lib", "ystrips"],
+    ap.add_argument("--order", default="lib", choices=["ylines", "none", "lib", "ystrips", "ystrips3", "ystrips4"],
                     help="lib: the library's own chunk order; ylines: workloads.chunk_order_ylines; none: storage")
     args = ap.parse_args()
     import torch
@@ -60,11 +60,12 @@ def main():
                     if args.order == "ylines" and ".bc." in name:
                         per_sm = 1 if R == 32 else (2 if R == 16 else 3)
                         ctx.set_chunk_order(chunk_order_ylines(lat, sms * per_sm))
-                    elif args.order == "ystrips" and ".bc." in name:
+                    elif args.order.startswith("ystrips") and ".bc." in name:
                         from workloads.ti_lattice import chunk_order_ystrips
 
                         per_sm = 1 if R == 32 else (2 if R == 16 else 3)
-                        ctx.set_chunk_order(chunk_order_ystrips(lat, sms * per_sm))
+                        width = int(args.order[7:] or 2)
+                        ctx.set_chunk_order(chunk_order_ystrips(lat, sms * per_sm, width=width))
                     elif args.order == "none":
                         ctx.set_chunk_order(np.arange(ctx.sell_info().n_chunks, dtype=np.int64))
                     ctx.moments(args.M, R, SEED, want_eta=False)

@@ -5,7 +5,7 @@ and without the multi-rank edge split, and is a permutation for any input."""
 import numpy as np
 import pytest
 
-from workloads.ti_lattice import Lattice, chunk_order_ylines, generate_csr
+from workloads.ti_lattice import Lattice, chunk_order_ylines, chunk_order_ystrips, generate_csr
 
 C = 32
 
@@ -60,13 +60,24 @@ def test_edges_last_matches(pkg, dims, grid):
     assert np.array_equal(got, chunk_order_ylines(lat, grid, edges_last=True))
 
 
+@pytest.mark.parametrize("dims,grid", [((200, 100, 40), 148), ((21, 12, 16), 10), ((8, 9, 8), 3)])
+def test_strip_walk_matches_ystrips(pkg, dims, grid):
+    """width 2: strips of two x-adjacent y-lines walked step by step (the R = 32 kernel's order)."""
+    lat = Lattice(*dims)
+    rp, col, _ = generate_csr(lat)
+    ptr, nbr = block_neighbours(rp, col, lat.n)
+    got = pkg.plan_chunk_order(ptr, nbr, grid, width=2)
+    assert np.array_equal(got, chunk_order_ystrips(lat, grid))
+
+
 def test_permutation_for_arbitrary_graphs(pkg):
     rng = np.random.default_rng(3)
     for n in (1, 5, 300):
         ptr = np.concatenate([[0], np.cumsum(rng.integers(0, 6, n))])
         nbr = rng.integers(0, n, ptr[-1])
         for grid in (1, 3, 148):
-            got = pkg.plan_chunk_order(ptr, nbr, grid)
-            assert np.array_equal(np.sort(got), np.arange(n))
+            for width in (1, 2):
+                got = pkg.plan_chunk_order(ptr, nbr, grid, width=width)
+                assert np.array_equal(np.sort(got), np.arange(n))
     with pytest.raises(pkg.KpmError):
         pkg.plan_chunk_order([0, 1], [5], 4)

@@ -82,11 +82,16 @@ def run_case(pkg, P, n, rp, col, val, bounds, M, R, seed, want_v0=False):
     v0 = rng.normal(size=(n, 2)) + 1j * rng.normal(size=(n, 2))
 
     def fn(ctx, r):
+        trace = os.environ.get("VRANKS_TRACE")
         r0, r1 = bounds[r], bounds[r + 1]
         lrp = rp[r0:r1 + 1] - rp[r0]
         lcol, lval = col[rp[r0]:rp[r1]], val[rp[r0]:rp[r1]]
         ctx.set_matrix(lrp, lcol, lval, a, b, n_global=n, row_begin=r0)
+        if trace:
+            print(f"rank {r}: set_matrix done", flush=True)
         mu, eta = ctx.moments(M, R, seed)
+        if trace:
+            print(f"rank {r}: moments done ({ctx.last_kernel()})", flush=True)
         res = dict(mu=mu, eta=eta, kernel=ctx.last_kernel(), sell=ctx.export_sell(), halo=ctx.export_halo(), lrp=lrp,
                    lcol=lcol, lval=lval)
         if want_v0:
@@ -154,7 +159,12 @@ def case_mismatch(pkg):
 
 
 def main():
+    import faulthandler
+
     import paper_1410_5242_b200 as pkg
+
+    if os.environ.get("VRANKS_DUMP_AFTER"):  # diagnostics: every thread's stack if a case hangs
+        faulthandler.dump_traceback_later(float(os.environ["VRANKS_DUMP_AFTER"]), exit=True)
 
     kind = sys.argv[1]
     try:

@@ -341,17 +341,18 @@ def chunk_order_ylines(lat: Lattice, grid: int, C: int = 32, x0: int = 0, x1: in
     return np.concatenate(parts).astype(np.int64)
 
 
-def chunk_order_ystrips(lat: Lattice, grid: int, C: int = 32, x0: int = 0, x1: int = None):
-    """Experiment (locality hint, not method arithmetic): like chunk_order_ylines, but each CTA
-    walks a strip of TWO x-adjacent y-lines step by step -- tiles (x, y), (x+1, y), (x, y+1),
-    (x+1, y+1), ... -- so that, besides the y-neighbours, every tile's x-neighbour on the strip's
-    inside is a block the CTA already holds.  Strips of lines (x, z), (x+1, z) for even x; rounds
-    of `grid` strips in lock step; the rest in storage order."""
+def chunk_order_ystrips(lat: Lattice, grid: int, C: int = 32, x0: int = 0, x1: int = None, width: int = 2):
+    """Locality hint (not method arithmetic): like chunk_order_ylines, but each CTA walks a strip
+    of `width` x-adjacent y-lines step by step -- tiles (x, y), (x+1, y), (x, y+1), (x+1, y+1), ...
+    for width 2 -- so that, besides the y-neighbours, every tile's x-neighbour on the strip's inside
+    is a block the CTA already holds.  Strips of lines (x..x+width-1, z) for x = 0, width, ...;
+    rounds of `grid` strips in lock step; the rest in storage order.  The library's own order
+    (kpm_plan_chunk_order, width 2) equals the width-2 form."""
     if (4 * lat.nz) % C:
         raise ValueError("needs 8 | Nz so chunks align with z-columns")
     zb = 4 * lat.nz // C
     nxl = (lat.nx if x1 is None else x1) - x0
-    strips = [(x, z) for x in range(0, nxl - 1, 2) for z in range(zb)]
+    strips = [(x, z) for x in range(0, nxl - width + 1, width) for z in range(zb)]
     rounds = len(strips) // grid
     parts, used = [], np.zeros(nxl * lat.ny * zb, dtype=bool)
     for r in range(rounds):
@@ -359,7 +360,7 @@ def chunk_order_ystrips(lat: Lattice, grid: int, C: int = 32, x0: int = 0, x1: i
         xs = np.array([x for x, _ in st])
         zs = np.array([z for _, z in st])
         for y in range(lat.ny):
-            for dx in (0, 1):
+            for dx in range(width):
                 ids = ((xs + dx) * lat.ny + y) * zb + zs
                 parts.append(ids)
                 used[ids] = True
