@@ -19,8 +19,8 @@ def main():
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--sigma", type=int, default=1)
     ap.add_argument("--variant", default="", help="kernel variant name (KPM_VARIANT by name)")
-    ap.add_argument("--order", default="ylines", choices=["ylines", "storage"],
-                    help="ylines: the bench's chunk order at R = 16 / 32 (block-cache feed)")
+    ap.add_argument("--order", default="lib", choices=["lib", "ylines", "storage"],
+                    help="lib: the library's own order; ylines: workloads.chunk_order_ylines; storage: forced")
     args = ap.parse_args()
     import paper_1410_5242_b200 as kpm
 
@@ -35,7 +35,11 @@ def main():
     with kpm.KpmContext(sell_sigma=args.sigma) as ctx:
         ctx.set_matrix(rp, col, val, a, b)
         for R in (int(r) for r in args.R.split(",")):
-            if args.order == "ylines":
+            if args.order == "storage":
+                import numpy as np
+
+                ctx.set_chunk_order(np.arange(ctx.sell_info().n_chunks, dtype=np.int64))
+            elif args.order == "ylines":
                 import torch
 
                 from workloads.ti_lattice import chunk_order_ylines
