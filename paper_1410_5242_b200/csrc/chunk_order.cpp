@@ -12,7 +12,8 @@
 // CTA b's k-th tile), interleaved so that all CTAs are at the same step: consecutive tiles of a
 // CTA then share their line-direction neighbour blocks (the block-cache feed keeps them in shared
 // memory) and the other neighbours are the current tiles of other CTAs (L2 hits).  Lines left
-// over after the last full round, and chunks in no line, follow in storage order.  Chunks with
+// over after the last full round, then chunks in no line, are cut into G balanced contiguous
+// segments, one per CTA, also walked in lock step.  Chunks with
 // skip[c] != 0 (the edge chunks of a multi-rank split) are kept out of the lines and go last.
 // width = 2 walks strips of two adjacent lines step by step (c, c', c + d, c' + d, ... with c' =
 // c + d2, d2 the next frequent offset: TI x): a tile's neighbour on the strip's inside is then a
@@ -107,6 +108,7 @@ std::vector<int64_t> line_order(int64_t n_chunks, const std::vector<int64_t>& pt
     // rounds of G units of equal length and kind (longest first, starts ascending inside a
     // length), all CTAs at the same step; a pair advances both of its lines per step
     std::stable_sort(units.begin(), units.end(), [](const auto& a, const auto& b) { return a[1] > b[1]; });
+    std::vector<int64_t> rest;  // walks of the units left over after the full rounds, in unit order
     size_t i = 0;
     while (i < units.size()) {
       size_t j = i;
@@ -120,12 +122,32 @@ std::vector<int64_t> line_order(int64_t n_chunks, const std::vector<int64_t>& pt
               order.push_back(c);
               used[c] = 1;
             }
+      for (size_t l = i + full; l < j; ++l)
+        for (int64_t step = 0; step < units[l][1]; ++step)
+          for (int lane = 0; lane < (units[l][2] >= 0 ? 2 : 1); ++lane) {
+            const int64_t c = (lane ? units[l][2] : units[l][0]) + step * d;
+            rest.push_back(c);
+            used[c] = 1;
+          }
       i = j;
     }
+    for (int64_t c = 0; c < n_chunks; ++c)  // chunks in no line
+      if (!used[c] && in(c)) rest.push_back(c);
+    // The rest in G balanced contiguous segments, one per CTA, walked in lock step (position
+    // base + k G + b = step k of CTA b): a CTA keeps walking its strip(s) instead of jumping
+    // through storage order (at 4 GPUs half of a C4 slab's strips are left over).
+    const int64_t n_left = (int64_t)rest.size(), K = n_left / G, rem = n_left % G;
+    std::vector<int64_t> seg(n_left);
+    for (int64_t b = 0; b < G; ++b) {
+      const int64_t start = b * K + std::min(b, rem), len = K + (b < rem ? 1 : 0);
+      for (int64_t k = 0; k < len; ++k) seg[k * G + b] = rest[start + k];
+    }
+    order.insert(order.end(), seg.begin(), seg.end());
+  } else {
+    for (int64_t c = 0; c < n_chunks; ++c)  // no line direction: storage order
+      if (in(c)) order.push_back(c);
   }
-  for (int64_t c = 0; c < n_chunks; ++c)  // leftover lines and chunks in no line, then skipped ones
-    if (!used[c] && in(c)) order.push_back(c);
-  for (int64_t c = 0; c < n_chunks; ++c)
+  for (int64_t c = 0; c < n_chunks; ++c)  // skipped chunks last
     if (!in(c)) order.push_back(c);
   return order;
 }

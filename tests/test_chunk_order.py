@@ -1,7 +1,8 @@
 """CPU tests of the library's default chunk order (kpm_plan_chunk_order, csrc/chunk_order.cpp;
-DESIGN.md §7 "Chunk order"): derived from the matrix's chunk adjacency alone, it reproduces the
-TI-specific y-line walk of round 1 (workloads.chunk_order_ylines) on the paper's lattices, with
-and without the multi-rank edge split, and is a permutation for any input."""
+DESIGN.md §7 "Chunk order"): derived from the matrix's chunk adjacency alone, it equals the
+TI-specific walks written out in workloads.ti_lattice (y-lines, 2-line strips; lock-step rounds
+of the launch grid, leftovers in balanced lock-step segments) on the paper's lattices, with and
+without the multi-rank edge split, and is a permutation for any input."""
 import numpy as np
 import pytest
 
@@ -35,7 +36,7 @@ def block_neighbours(rp, col, n):
 
 
 @pytest.mark.parametrize("dims,grid", [((200, 100, 40), 148), ((20, 12, 16), 148), ((30, 7, 8), 16), ((9, 40, 24), 7)])
-def test_line_walk_matches_round1_ylines(pkg, dims, grid):
+def test_line_walk_matches_ylines_twin(pkg, dims, grid):
     lat = Lattice(*dims)
     rp, col, _ = generate_csr(lat)
     ptr, nbr = block_neighbours(rp, col, lat.n)

@@ -308,13 +308,26 @@ def chunk_order_yband(lat: Lattice, x0: int, x1: int, band: int, C: int = 32):
     return np.concatenate(order).astype(np.int64)
 
 
+def _lockstep_segments(rest: np.ndarray, grid: int) -> np.ndarray:
+    """The chunks left after the full rounds, cut into `grid` balanced contiguous segments (CTA b
+    gets rest[start_b : start_b + len_b]) and laid out so that list position k*grid + b is step k
+    of CTA b (the library's rule, csrc/chunk_order.cpp)."""
+    n = len(rest)
+    K, rem = divmod(n, grid)
+    out = np.empty(n, dtype=np.int64)
+    for b in range(grid):
+        start, ln = b * K + min(b, rem), K + (1 if b < rem else 0)
+        out[np.arange(ln) * grid + b] = rest[start:start + ln]
+    return out
+
+
 def chunk_order_ylines(lat: Lattice, grid: int, C: int = 32, x0: int = 0, x1: int = None, edges_last: bool = False):
     """Locality hint for kpm_set_chunk_order and the block-cache feed (not method arithmetic):
     list position b + grid*k is CTA b's k-th tile.  In full rounds of `grid` lines, CTA b
     walks one y-line of chunks (x, 0..Ny-1, z-block), all CTAs in step at the same y, so
     consecutive tiles of a CTA share their y-neighbour blocks and the x-neighbour blocks are
-    other CTAs' current own blocks (L2 hits).  The lines left over after the last full round
-    follow in storage order (no reuse, perfect balance).  Chunk ids are local to the x-slab
+    other CTAs' current own blocks (L2 hits).  The lines left over after the last full round are
+    cut into `grid` balanced contiguous segments walked in lock step.  Chunk ids are local to the x-slab
     [x0, x1); with edges_last (several ranks) the slab's first and last x-planes -- the edge
     chunks, launched separately -- go to the end, so the interior list keeps the rounds."""
     if (4 * lat.nz) % C:
@@ -333,7 +346,7 @@ def chunk_order_ylines(lat: Lattice, grid: int, C: int = 32, x0: int = 0, x1: in
     rest = lines[rounds * grid:]
     if len(rest):
         x, z = rest // zb, rest % zb
-        parts.append(np.sort(((x[:, None] * lat.ny + y[None, :]) * zb + z[:, None]).ravel()))
+        parts.append(_lockstep_segments(((x[:, None] * lat.ny + y[None, :]) * zb + z[:, None]).ravel(), grid))
     if edges_last and nxl > 2:
         ex = np.array([0, nxl - 1])
         parts.append(np.sort(((ex[:, None, None] * lat.ny + y[None, :, None]) * zb
@@ -346,8 +359,9 @@ def chunk_order_ystrips(lat: Lattice, grid: int, C: int = 32, x0: int = 0, x1: i
     of `width` x-adjacent y-lines step by step -- tiles (x, y), (x+1, y), (x, y+1), (x+1, y+1), ...
     for width 2 -- so that, besides the y-neighbours, every tile's x-neighbour on the strip's inside
     is a block the CTA already holds.  Strips of lines (x..x+width-1, z) for x = 0, width, ...;
-    rounds of `grid` strips in lock step; the rest in storage order.  The library's own order
-    (kpm_plan_chunk_order, width 2) equals the width-2 form."""
+    rounds of `grid` strips in lock step; the leftover strips, then lines in no strip, in `grid`
+    balanced lock-step segments.  The library's own order (kpm_plan_chunk_order, width 2)
+    equals the width-2 form."""
     if (4 * lat.nz) % C:
         raise ValueError("needs 8 | Nz so chunks align with z-columns")
     zb = 4 * lat.nz // C
@@ -364,7 +378,13 @@ def chunk_order_ystrips(lat: Lattice, grid: int, C: int = 32, x0: int = 0, x1: i
                 ids = ((xs + dx) * lat.ny + y) * zb + zs
                 parts.append(ids)
                 used[ids] = True
-    parts.append(np.nonzero(~used)[0])
+    rest = []
+    for x, z in strips[rounds * grid:]:  # leftover strips, each walked step by step
+        ids = ((x + np.arange(width)[None, :]) * lat.ny + np.arange(lat.ny)[:, None]) * zb + z
+        rest.append(ids.ravel())
+        used[ids.ravel()] = True
+    rest.append(np.nonzero(~used)[0])
+    parts.append(_lockstep_segments(np.concatenate(rest).astype(np.int64), grid))
     return np.concatenate(parts).astype(np.int64)
 
 
