@@ -256,6 +256,13 @@ def main():
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if world > 1 and "NCCL_DEBUG" not in os.environ:
+        # communicator INIT lines (ranks, NVLS/P2P transports) go to stderr with everything the
+        # native libraries print during setup (below); stdout stays the one JSON line.  Set
+        # before the first NCCL call (ncclGetUniqueId on rank 0): NCCL reads it once.
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # NCCL logs to stdout otherwise
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
 
@@ -309,18 +316,13 @@ def main():
     a, b = scale_factors(lo, hi)
     n, nnz = lat.n, lat.nnz_expected()
     uid = None
-    if world > 1:
-        box = [kpm.get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(box, src=0)
-        uid = box[0]
-    if world > 1 and "NCCL_DEBUG" not in os.environ:
-        # communicator INIT lines (ranks, NVLS/P2P transports) go to stderr with everything the
-        # native libraries print during setup (below); stdout stays the one JSON line
-        os.environ["NCCL_DEBUG"] = "INFO"
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     saved = os.dup(1)
     os.dup2(2, 1)  # anything the native libraries print during setup goes to stderr
     try:
+        if world > 1:
+            box = [kpm.get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0)
+            uid = box[0]
         ctx = kpm.KpmContext(device=local, nranks=world, rank=rank, nccl_unique_id=uid,
                              cuda_stream=stream.cuda_stream)
     finally:

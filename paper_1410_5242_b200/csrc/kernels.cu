@@ -449,10 +449,7 @@ __host__ __device__ constexpr int tiled_threads() { return 32 * (tiled_ncwg<LPR>
 // BC: block-cache feed: records per list position, V rows of a tile live in a
 // pool of 32-row blocks kept across the CTA's tiles (plus per-stage extra rows), lcol holds
 // absolute shared-memory V rows, the header carries the own block's first row.
-// A2: the full batches accumulate odd entries into a second partial sum (added at the end), which
-// halves the length of the dependent DFMA chains per accumulator (summation order only).
-template <int R, int LPR, int U, int CS, bool WS, bool INIT, int KIND = kAug, int MINB = 1, bool BC = false,
-          bool A2 = false>
+template <int R, int LPR, int U, int CS, bool WS, bool INIT, int KIND = kAug, int MINB = 1, bool BC = false>
 __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tiled(const SweepArgs a) {
   using Cf = Cfg<R, LPR, U>;
   constexpr int RW = Cf::RW, G = kC / RW;
@@ -586,9 +583,6 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
           j = 1;
         }
         const bool own0 = PEEL && li0 == (own_row + kr) * R;
-        double2 u2[A2 ? CPL : 1];
-#pragma unroll
-        for (int cc = 0; cc < (A2 ? CPL : 1); ++cc) u2[cc] = make_double2(0.0, 0.0);
         for (; j + U <= L; j += U) {  // full batches: no predication
           double2 h[U];
           int li[U];
@@ -605,19 +599,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
 #pragma unroll
           for (int uu = 0; uu < U; ++uu)
 #pragma unroll
-            for (int cc = 0; cc < CPL; ++cc) {
-              if (A2 && (uu & 1))
-                cmac(u2[A2 ? cc : 0], h[uu], x[uu][cc]);
-              else
-                cmac(u[cc], h[uu], x[uu][cc]);
-            }
-        }
-        if (A2) {
-#pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) {
-            u[cc].x += u2[A2 ? cc : 0].x;
-            u[cc].y += u2[A2 ? cc : 0].y;
-          }
+            for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h[uu], x[uu][cc]);
         }
         for (; j < L; ++j) {
           const double2 h = sv[j * kC];
@@ -702,7 +684,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
 
 enum Feed { kDirect = 0, kStaged = 1, kTiled = 2 };
 
-template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true, int MINB = 1, bool BC = false, bool A2 = false>
+template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true, int MINB = 1, bool BC = false>
 struct Variant {
   static cudaError_t launch(bool init, const SweepArgs& a, int grid, cudaStream_t s) {
     if constexpr (FEED == kStaged) {
@@ -712,8 +694,8 @@ struct Variant {
         aug_spmmv_staged<R, LPR, U, false><<<grid, kThreads, kStagedSmem, s>>>(a);
     } else if constexpr (FEED == kTiled) {
       const int smem = a.tl.pool_bytes + a.tl.stages * a.tl.stage_bytes;
-      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB, BC, A2>;
-      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB, BC, A2>;
+      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB, BC>;
+      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB, BC>;
       cudaFuncSetAttribute(k_init, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       (init ? k_init : k_main)<<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
@@ -735,8 +717,8 @@ struct Variant {
       cudaFuncGetAttributes(&fa, aug_spmmv_staged<R, LPR, U, true>);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_staged<R, LPR, U, false>, kThreads, kStagedSmem);
     } else if constexpr (FEED == kTiled) {
-      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB, BC, A2>;
-      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB, BC, A2>;
+      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB, BC>;
+      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB, BC>;
       cudaFuncSetAttribute(k_init, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
       cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_main, tiled_threads<LPR, CS>(), dyn_smem);
@@ -802,8 +784,6 @@ const Entry kTable[] = {
     // 4-lane map under the power cap (profiles/r02_variants/)
     {16, "tiled.bc.lpr8.u4.wr", kTiled, false, Variant<16, 8, 4, kTiled, 1, false, 2, true>::launch,
      Variant<16, 8, 4, kTiled, 1, false, 2, true>::occupancy, 2, 2},
-    {16, "tiled.bc.lpr8.u4.wr.a2", kTiled, false, Variant<16, 8, 4, kTiled, 1, false, 2, true, true>::launch,
-     Variant<16, 8, 4, kTiled, 1, false, 2, true, true>::occupancy, 2, 2},
     {16, "tiled.bc.lpr4.u4.wr", kTiled, false, Variant<16, 4, 4, kTiled, 1, false, 2, true>::launch,
      Variant<16, 4, 4, kTiled, 1, false, 2, true>::occupancy, 2, 2},
     KPM_VARIANT_WR_S(16, 4, 4, 2, "tiled.lpr4.u4.wr.s2"),
@@ -818,8 +798,6 @@ const Entry kTable[] = {
     // R = 32: walked in strips of two lines (-2 % under the power cap, profiles/r02_variants/)
     {32, "tiled.bc.lpr8.u4", kTiled, true, Variant<32, 8, 4, kTiled, 1, true, 1, true>::launch,
      Variant<32, 8, 4, kTiled, 1, true, 1, true>::occupancy, 2, 1, 2},
-    {32, "tiled.bc.lpr8.u4.a2", kTiled, true, Variant<32, 8, 4, kTiled, 1, true, 1, true, true>::launch,
-     Variant<32, 8, 4, kTiled, 1, true, 1, true, true>::occupancy, 2, 1, 2},
     KPM_VARIANT(32, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT_WR(32, 8, 4, "tiled.lpr8.u4.wr"),
     KPM_VARIANT_CS(32, 8, 4, 2, "tiled.lpr8.u4.cs2"),

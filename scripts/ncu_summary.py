@@ -25,7 +25,11 @@ KEYS = [
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """Metrics of an ncu report (.ncu-rep) or of its `ncu -i ... --page raw --csv` export (.csv)."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return {h: (u, v) for h, u, v in zip(rows[0], rows[1], rows[2])}
 
