@@ -256,7 +256,7 @@ def main():
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
-    if world > 1 and "NCCL_DEBUG" not in os.environ:
+    if world > 1 and os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", "WARN"):  # image default: VERSION
         # communicator INIT lines (ranks, NVLS/P2P transports) go to stderr with everything the
         # native libraries print during setup (below); stdout stays the one JSON line.  Set
         # before the first NCCL call (ncclGetUniqueId on rank 0): NCCL reads it once.

@@ -1,8 +1,9 @@
 """Fig. 1-scale demo: DOS of the 1600 x 1600 x 40 topological
 insulator (N = 4.1e8; Fig. 1 `topi_dos`) on the GPUs of one box, with
 the x-slab distribution and the fused NVLink halo exchange; Jackson-kernel reconstruction.
-Run with torchrun (one rank per GPU).  Rank 0 writes gpurun_out/fig1_dos.csv and prints a
-JSON summary."""
+Run with torchrun (one rank per GPU).  The chunk order is the library's own.  Rank 0 writes
+the DOS curve (--out, default gpurun_out/fig1_dos.csv) and prints a JSON summary;
+tests/test_gpu_parity.py runs it on a small lattice on one GPU."""
 import argparse
 import json
 import os
@@ -15,8 +16,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
-from workloads.ti_lattice import (SEED, Lattice, chunk_order_yband, gershgorin, generate_csr,  # noqa: E402
-                                  generate_csr_torch, scale_factors)
+from workloads.ti_lattice import SEED, Lattice, gershgorin, generate_csr, generate_csr_torch, scale_factors  # noqa: E402
 
 
 def main():
@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--lattice", default="1600,1600,40")
     ap.add_argument("--M", type=int, default=2000)
     ap.add_argument("--R", type=int, default=32)
+    ap.add_argument("--out", default="gpurun_out/fig1_dos.csv")
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -50,15 +51,14 @@ def main():
     ctx.set_matrix(rp, col, val, a, b, n_global=lat.n, row_begin=x0 * lat.rows_per_plane, mem=kpm.KPM_MEM_DEVICE)
     del rp, col, val
     torch.cuda.empty_cache()
-    ctx.set_chunk_order(chunk_order_yband(lat, x0, x1, 97))
     t_setup = time.time() - t0
     mu, _ = ctx.moments(args.M, args.R, SEED, want_eta=False)
     total_ms, sweep_ms, _ = ctx.last_timing()
     ctx.close()
     if rank == 0:
         E, rho = kpm.dos(mu, a, b, K=4000)
-        os.makedirs("gpurun_out", exist_ok=True)
-        np.savetxt("gpurun_out/fig1_dos.csv", np.stack([E, rho], 1), delimiter=",", header="E,rho(E)")
+        os.makedirs(os.path.dirname(os.path.abspath(args.out)), exist_ok=True)
+        np.savetxt(args.out, np.stack([E, rho], 1), delimiter=",", header="E,rho(E)")
         x = a * (E - b)
         integral = np.pi / len(x) * np.sum(rho / a * np.sqrt(1 - x * x))
         nnz = lat.nnz_expected()

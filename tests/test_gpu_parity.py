@@ -601,3 +601,22 @@ def test_per_sweep_timing(pkg):
         ctx.set_matrix(rp, col, val, a, b)
         ctx.moments(64, 4, SEED)
         assert len(ctx.sweep_times()) == 0
+
+
+def test_fig1_demo_small(pkg, tmp_path):
+    """The Fig. 1 demo (scripts/fig1_demo.py) end to end on one GPU at a small
+    size: device-generated CSR, library order, Jackson DOS; mu_0 = N and the DOS integrates to N."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    out = tmp_path / "dos.csv"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, f"{root}/scripts/fig1_demo.py", "--lattice", "40,40,40", "--M", "200",
+                          "--R", "8", "--out", str(out)], capture_output=True, text=True, timeout=600, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    d = json.loads([l for l in res.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["mu0"] == d["N"] == 4 * 40 * 40 * 40
+    assert d["integral_rho"] == pytest.approx(d["N"], rel=1e-9)
+    assert out.exists()
