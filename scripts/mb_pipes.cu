@@ -1,57 +1,74 @@
-// Microbenchmark (round 2): do texture fetches and shared-memory loads share the
-// register-side data path of the SM?  Warps either stream LDS.128 from shared memory, or fetch
-// 16-B texels (tex1Dfetch<int4>) of a small L1-resident buffer, or both kinds side by side in
-// one CTA; bytes delivered to registers per SM clock for each mix.  Build and run:
+// Microbenchmark (round 2): do texture fetches / L1-hit global loads and shared-memory
+// loads share the register-side data path of the SM?  One CTA of W warps per SM; each warp runs
+// either LDS.128 from shared memory or TLD (tex1Dfetch<int4>) / LDG.E.128.CONSTANT of an
+// L1-resident 16-KB buffer, 8 independent 16-B loads in flight per thread.  Each warp's cycles are
+// recorded; the line reports bytes per SM clock for each warp class and in total.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb_pipes scripts/mb_pipes.cu && /tmp/mb_pipes
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
 
-constexpr int kIters = 4096;
+constexpr int kIters = 2048;
+constexpr int kILP = 8;
 
-// mode 0: all warps LDS; 1: all warps TEX; 2: even warps LDS, odd warps TEX; 3: all warps LDG.nc
-__global__ void __launch_bounds__(512) mix(cudaTextureObject_t tex, const int4* __restrict__ g, int n_tex, int mode,
-                                          int4* out, long long* clk) {
+enum { kLds = 0, kTex = 1, kLdg = 2 };
+
+// kind of warp w for a mix: 0 all LDS; 1 all TEX; 2 all LDG; 3 LDS/TEX alternating; 4 LDS/LDG alternating
+__device__ __forceinline__ int warp_kind(int mix, int w) {
+  if (mix <= 2) return mix;
+  return (w & 1) ? (mix == 3 ? kTex : kLdg) : kLds;
+}
+
+__global__ void __launch_bounds__(1024) bench(cudaTextureObject_t tex, const int4* __restrict__ g, int mix, int4* out,
+                                              long long* clk) {
   __shared__ int4 sm[2048];  // 32 KB
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) sm[i] = make_int4(i, i + 1, i + 2, i + 3);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool use_tex = mode == 1 || (mode == 2 && (warp & 1));
-  const bool use_ldg = mode == 3;
-  int4 acc = make_int4(0, 0, 0, 0);
-  unsigned idx = (threadIdx.x * 7u) & 2047u;
+  const int kind = warp_kind(mix, warp);
+  int4 acc[kILP];
+#pragma unroll
+  for (int k = 0; k < kILP; ++k) acc[k] = make_int4(0, 0, 0, 0);
+  const unsigned base = (unsigned)(warp * 64 + lane);
   const long long t0 = clock64();
-#pragma unroll 8
   for (int it = 0; it < kIters; ++it) {
-    int4 v;
-    if (use_tex)
-      v = tex1Dfetch<int4>(tex, (int)(idx & (unsigned)(n_tex - 1)));
-    else if (use_ldg)
-      v = __ldg(g + (idx & (unsigned)(n_tex - 1)));
-    else
-      v = sm[idx];
-    acc.x += v.x;
-    acc.y ^= v.y;
-    acc.z += v.z;
-    acc.w ^= v.w;
-    idx = (idx + 32u) & 2047u;  // independent of the loaded data: loads overlap (throughput, not latency)
+    int4 v[kILP];
+#pragma unroll
+    for (int k = 0; k < kILP; ++k) {
+      const unsigned idx = (base + 32u * (unsigned)(it * kILP + k)) & 1023u;  // 32 distinct 16-B words per warp
+      if (kind == kTex)
+        v[k] = tex1Dfetch<int4>(tex, (int)idx);
+      else if (kind == kLdg)
+        v[k] = __ldg(g + idx);
+      else
+        v[k] = sm[idx];
+    }
+#pragma unroll
+    for (int k = 0; k < kILP; ++k) {
+      acc[k].x += v[k].x;
+      acc[k].y ^= v[k].y;
+      acc[k].z += v[k].z;
+      acc[k].w ^= v[k].w;
+    }
   }
   const long long t1 = clock64();
-  if (acc.x == 0x7fffffff) out[0] = acc;
-  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
-  (void)lane;
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < kILP; ++k) s += acc[k].x + acc[k].y + acc[k].z + acc[k].w;
+  if (s == 0x7fffffff) out[0] = acc[0];
+  if (lane == 0) clk[blockIdx.x * 32 + warp] = t1 - t0;
 }
 
 int main() {
-  const int n_tex = 1024;  // 16 KB of texels: L1-resident
+  const int n = 1024;  // 16 KB of texels / words: L1-resident
   int4* g;
-  cudaMalloc(&g, n_tex * sizeof(int4));
-  cudaMemset(g, 1, n_tex * sizeof(int4));
+  cudaMalloc(&g, n * sizeof(int4));
+  cudaMemset(g, 1, n * sizeof(int4));
   cudaResourceDesc rd = {};
   rd.resType = cudaResourceTypeLinear;
   rd.res.linear.devPtr = g;
   rd.res.linear.desc = cudaCreateChannelDesc<int4>();
-  rd.res.linear.sizeInBytes = n_tex * sizeof(int4);
+  rd.res.linear.sizeInBytes = n * sizeof(int4);
   cudaTextureDesc td = {};
   td.readMode = cudaReadModeElementType;
   cudaTextureObject_t tex;
@@ -61,26 +78,28 @@ int main() {
   int4* out;
   long long* clk;
   cudaMalloc(&out, 16);
-  cudaMalloc(&clk, sizeof(long long) * sms);
-  const char* names[] = {"LDS.128 only", "TEX (tex1Dfetch int4) only", "LDS + TEX (half the warps each)",
-                         "LDG.nc (L1 hits) only"};
-  for (int warps : {8, 16}) {
-    for (int mode = 0; mode < 4; ++mode) {
-      mix<<<sms, 32 * warps>>>(tex, g, n_tex, mode, out, clk);  // warm-up
-      cudaEvent_t e0, e1;
-      cudaEventCreate(&e0);
-      cudaEventCreate(&e1);
-      cudaEventRecord(e0);
-      mix<<<sms, 32 * warps>>>(tex, g, n_tex, mode, out, clk);
-      cudaEventRecord(e1);
-      cudaEventSynchronize(e1);
-      float ms = 0;
-      cudaEventElapsedTime(&ms, e0, e1);
-      long long c = 0;
-      cudaMemcpy(&c, clk, sizeof(long long), cudaMemcpyDeviceToHost);
-      const double bytes_per_sm = 32.0 * warps * 16.0 * kIters;
-      printf("{\"warps\": %d, \"mode\": \"%s\", \"cycles\": %lld, \"bytes_per_clk_per_sm\": %.1f, \"ms\": %.4f}\n", warps,
-             names[mode], c, bytes_per_sm / (double)c, ms);
+  cudaMalloc(&clk, sizeof(long long) * sms * 32);
+  const char* names[] = {"LDS only", "TEX only", "LDG.nc only", "LDS + TEX", "LDS + LDG.nc"};
+  for (int warps : {16, 32}) {
+    for (int mix = 0; mix < 5; ++mix) {
+      bench<<<sms, 32 * warps>>>(tex, g, mix, out, clk);  // warm-up
+      bench<<<sms, 32 * warps>>>(tex, g, mix, out, clk);
+      cudaDeviceSynchronize();
+      long long c[32];
+      cudaMemcpy(c, clk, sizeof(long long) * 32, cudaMemcpyDeviceToHost);  // block 0
+      // per class: bytes moved by that class's warps / the slowest of them; total over the CTA
+      double bytes[3] = {0, 0, 0};
+      long long cmax[3] = {1, 1, 1}, call = 1;
+      for (int w = 0; w < warps; ++w) {
+        const int k = mix <= 2 ? mix : ((w & 1) ? (mix == 3 ? kTex : kLdg) : kLds);
+        bytes[k] += 32.0 * 16.0 * kILP * kIters;
+        if (c[w] > cmax[k]) cmax[k] = c[w];
+        if (c[w] > call) call = c[w];
+      }
+      printf("{\"warps\": %d, \"mix\": \"%s\", \"lds_B_per_clk\": %.1f, \"tex_B_per_clk\": %.1f, \"ldg_B_per_clk\": %.1f, "
+             "\"total_B_per_clk\": %.1f}\n",
+             warps, names[mix], bytes[0] / cmax[0], bytes[1] / cmax[1], bytes[2] / cmax[2],
+             (bytes[0] + bytes[1] + bytes[2]) / call);
     }
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
