@@ -121,21 +121,18 @@ kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt);
  * KPM_CHECK_HERMITIAN.  Replaces any previous matrix. */
 kpm_status kpm_set_matrix(kpm_ctx* ctx, const kpm_csr* H, double a, double b);
 
-/* Optional locality hint: the order in which the sweep kernels visit the n = n_chunks SELL
- * chunks (a permutation of 0..n_chunks-1, host array; NULL restores storage order).  The
- * moments are unchanged up to the rounding of the eta sums (which stay deterministic).  For
- * stencil matrices whose neighbour window exceeds L2 (e.g. the 400x400x40 TI at R = 32,
- * 65 MB), a banded order keeps the gathered rows L2-resident.
+/* Optional override of the order in which the sweep kernels visit the n = n_chunks SELL chunks
+ * (a permutation of 0..n_chunks-1, host array; NULL returns to the library's own choice).  The
+ * moments are unchanged up to the rounding of the eta sums (which stay deterministic).
  * Position i of the order is tile i / G of CTA i mod G (G = grid of the sweep launch, the SM
  * count times the CTAs per SM of the width's kernel; with several ranks the order is split
- * into the edge and the interior list, each keeping its relative order).  The block-cache
- * feed (R = 16, 32) reuses V blocks between a CTA's consecutive tiles, so an order in which
- * they are neighbours cuts its copies by 40 %.
- * Without a call (or after order = NULL) the library picks the order itself: for the
- * block-cache kernels, and for any kernel when the matrix's neighbour window exceeds 32 MB,
- * the line walk of kpm_plan_chunk_order derived from the matrix's chunk adjacency; otherwise
- * storage order.  Pass the identity permutation to force storage order.
- * Reset by kpm_set_matrix. */
+ * into the edge and the interior list, each keeping its relative order).
+ * Without a call the library picks the order itself (DESIGN.md §7 "Chunk order"): for the
+ * block-cache kernels (R = 16, 32), which reuse V blocks between a CTA's consecutive tiles, and
+ * for any kernel when the matrix's storage-order neighbour window exceeds 32 MB (e.g. the
+ * 400x400x40 TI at R = 32: 65 MB), the lock-step line / strip walk of kpm_plan_chunk_order derived
+ * from the matrix's chunk adjacency; otherwise storage order.  Pass the identity permutation
+ * to force storage order.  Reset by kpm_set_matrix. */
 kpm_status kpm_set_chunk_order(kpm_ctx* ctx, const int64_t* order, int64_t n);
 
 /* KPM-DOS moments with R random start vectors |rand()>: Z4 phases
