@@ -1177,7 +1177,10 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   int variant = 0, grid = 1;
   TileLayout tl;
   bool bc = false;
-  if ((st = select_variant(ctx, Rk, variant, tl, grid, bc)) != KPM_OK) return st;
+  st = select_variant(ctx, Rk, variant, tl, grid, bc);
+  // a local failure after the (cached) choice must not leave the other ranks in the next collective
+  if (ctx->opt.nranks > 1 && !ctx->sticky) st = agree(ctx, st);
+  if (st != KPM_OK) return st;
   KPM_TRACE_LINE(ctx->opt.rank, "variant selected: %s (fused %d, edge %lld, interior %lld)", variant_name(Rk, variant),
                  (int)ctx->fused, (long long)ctx->n_edge, (long long)ctx->n_interior);
   const int rec_index = 2 * __builtin_ctz(Rk) + (variant_wstage(Rk, variant) ? 1 : 0);
