@@ -119,7 +119,6 @@ struct kpm_ctx {
   // multi-rank (nranks > 1): row distribution, halo exchange plan, NCCL
   ncclComm_t comm = nullptr;
   kpm_vgroup* vg = nullptr;         // virtual ranks (no NCCL): the in-process group
-  std::vector<int64_t> peer_x0, peer_x1;  // virtual ranks: every rank's X0 / X1 (device pointers)
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_edge = nullptr, ev_halo = nullptr;
   std::vector<int64_t> row_begins;  // nranks+1
