@@ -82,3 +82,18 @@ def test_permutation_for_arbitrary_graphs(pkg):
                 assert np.array_equal(np.sort(got), np.arange(n))
     with pytest.raises(pkg.KpmError):
         pkg.plan_chunk_order([0, 1], [5], 4)
+
+
+def test_leftover_segments_balanced(pkg):
+    """Lines left after the last full round are cut into `grid` contiguous, balanced segments:
+    CTA b (positions b, b + G, ... after the rounds) walks consecutive chunks of one line."""
+    lat = Lattice(7, 10, 8)  # 7 lines of length 10 (zb = 1): with G = 3, 2 rounds + 1 line left
+    rp, col, _ = generate_csr(lat)
+    ptr, nbr = block_neighbours(rp, col, lat.n)
+    G = 3
+    got = pkg.plan_chunk_order(ptr, nbr, G)
+    rest = got[2 * 3 * 10:]  # after 2 rounds of 3 lines x 10 steps
+    per_cta = [rest[b::G] for b in range(G)]
+    assert sorted(len(p) for p in per_cta) == [3, 3, 4]
+    for p in per_cta:  # each segment: consecutive y-steps of the leftover line (chunk offset 1)
+        assert np.all(np.diff(p) == 1)

@@ -38,3 +38,16 @@ def test_c3_numbers_of_the_survey(bench):
     nnz = 13 * n - 16 * 200 * 100
     assert bench.alg_bytes_per_sweep(n, nnz, 32) == 5_740_800_000
     assert bench.alg_flops_per_sweep(n, nnz, 32) == pytest.approx(14.049e9, rel=1e-4)
+
+
+def test_both_arms_emit_the_same_config(bench):
+    """bench.py's reference arm and its own arm build `config` with one function (the driver's
+    same_config check)."""
+    import argparse
+
+    for cfg, world in (("bar", 1), ("bar", 4), ("C4", 2)):
+        args = argparse.Namespace(config=cfg, lattice="200,100,40", M=None, R=None)
+        w = bench.workload(args, world)
+        c = bench.config_dict(w, world)
+        assert c["workload"] == w["name"] and c["parallelism"] == f"x-slab dp{world}"
+        assert set(c) == {"workload", "lattice", "M", "R", "parallelism"}
