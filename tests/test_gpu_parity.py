@@ -620,3 +620,35 @@ def test_fig1_demo_small(pkg, tmp_path):
     assert d["mu0"] == d["N"] == 4 * 40 * 40 * 40
     assert d["integral_rho"] == pytest.approx(d["N"], rel=1e-9)
     assert out.exists()
+
+
+@pytest.mark.parametrize("R", [1, 8, 32])
+def test_degenerate_sizes(pkg, R):
+    """Degenerate cases of the method: a 1x1 matrix (one chunk of 31 padding rows), M = 2 (the
+    init sweep only, mu = (eta_0, eta_1)), M = 4 (one main sweep, no CUDA graph), a matrix with
+    empty rows and a row of only a diagonal; each against the oracle."""
+    cases = []
+    cases.append((np.array([0, 1]), np.array([0]), np.array([0.3 + 0j]), 0.9, 0.1))  # H = (0.3)
+    n = 70  # a tridiagonal chain with rows 5 and 40 empty, row 63 a lone diagonal
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        if i in (5, 40):
+            continue
+        if i == 63:
+            rows.append(i), cols.append(i), vals.append(0.7 + 0j)
+            continue
+        for j, v in ((i - 1, 0.5 - 0.25j), (i + 1, 0.5 + 0.25j)):
+            if 0 <= j < n and j not in (5, 40, 63):
+                rows.append(i), cols.append(j), vals.append(v)
+    rows, cols, vals = np.array(rows), np.array(cols), np.array(vals, dtype=np.complex128)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rp, rows + 1, 1)
+    cases.append((np.cumsum(rp), cols.astype(np.int64), vals, 0.45, 0.0))
+    for rp, col, val, a, b in cases:
+        for M in (2, 4, 30):
+            with pkg.KpmContext() as ctx:
+                ctx.set_matrix(rp, col, val, a, b)
+                mu, eta = ctx.moments(M, R, SEED)
+            eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, SEED)
+            check(eta, mu, eta_o)
+            assert mu[0] == len(rp) - 1
