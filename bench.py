@@ -106,6 +106,30 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
+def cache_roofline(n_loc, nnz_loc, R, sm_mhz, sweep_ms, hbm_gbs, wavefronts):
+    """The shared-memory ceiling of the sweep, independent of the kernel's own instruction count:
+    the method needs at least every stored nonzero's V row (16 R bytes) delivered to registers
+    (the row is gathered once per nonzero), and the SM's shared-memory data path
+    delivers at most the LDS.128 peak measured by scripts/mb_lds_peak.cu
+    (profiles/r02_lds_peak.json) per clock, at the SM clock sampled during the timed region."""
+    p = os.path.join(ROOT, "profiles", "r02_lds_peak.json")
+    if not os.path.exists(p) or not sm_mhz:
+        return None
+    peak = float(json.load(open(p))["peak_lds128_B_per_clk_per_sm"])
+    sms = 148
+    min_bytes = nnz_loc * 16.0 * R
+    t_smem = min_bytes / (sms * peak * sm_mhz * 1e6) * 1e3
+    t_hbm = alg_bytes_per_sweep(n_loc, nnz_loc, R) / (hbm_gbs * 1e9) * 1e3
+    out = {"bound": "smem" if t_smem > t_hbm else "hbm", "peak_B_per_clk_per_sm": peak,
+           "peak_source": "measured (scripts/mb_lds_peak.cu, profiles/r02_lds_peak.json)",
+           "min_register_bytes_per_launch": min_bytes, "sm_mhz": sm_mhz, "t_smem_min_ms": t_smem,
+           "t_hbm_min_ms": t_hbm, "t_measured_ms": sweep_ms, "frac_of_applicable": max(t_smem, t_hbm) / sweep_ms}
+    if wavefronts:  # the kernel's own register-side traffic (ncu), for context only
+        out["kernel_register_bytes_per_launch"] = wavefronts * 128.0
+        out["kernel_over_min"] = wavefronts * 128.0 / min_bytes
+    return out
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -374,10 +398,12 @@ def main():
     bytes_sweep = alg_bytes_per_sweep(n_loc, nnz_loc, R)  # per rank per launch
     achieved = bytes_sweep / (sweep * 1e-3) / 1e9
     bmin = alg_bytes_per_sweep(n, nnz, R) / alg_flops_per_sweep(n, nnz, R)
-    traffic = None
+    traffic, smem_wf = None, None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
-        traffic = json.load(open(tf)).get(f"{px}x{ny}x{nz}/R{R}")
+        tj = json.load(open(tf))
+        traffic = tj.get(f"{px}x{ny}x{nz}/R{R}")
+        smem_wf = tj.get(f"{px}x{ny}x{nz}/R{R}/smem_wavefronts")
     out = {
         "metric": "augmented SpMMV Gflop/s (cplx dbl)", "value": value, "unit": "Gflop/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
@@ -399,6 +425,7 @@ def main():
         "gpu_launches": args.steps * n_blocks * ((M // 2) * (2 if world > 1 else 1) + 2),
         "clocks": clocks,
     }
+    out["cache_roofline"] = cache_roofline(n_loc, nnz_loc, R, clocks.get("sm_mhz"), sweep, hbm, smem_wf)
     # R sweep of the same lattice (HBM -> cache bottleneck shift), shorter M
     if not args.no_r_sweep and world == 1:
         by_r = {}
