@@ -344,6 +344,7 @@ def test_rows_without_diagonal(pkg, R):
 
 @pytest.mark.parametrize("ordered", [False, True])
 @pytest.mark.parametrize("R,dims,name,ctas", [(32, (40, 20, 32), "tiled.bc.lpr8.u4", 1),
+                                             (16, (80, 12, 32), "tiled.bc.lpr8.u4.wr", 2),
                                              (16, (80, 12, 32), "tiled.bc.lpr4.u4.wr", 2),
                                              (8, (120, 8, 32), "tiled.bc.lpr4.u4.wr", 3)])
 def test_block_cache_feed(pkg, monkeypatch, ordered, R, dims, name, ctas):
@@ -527,6 +528,22 @@ def test_check_hermitian_flag(pkg):
         assert e.value.status == pkg.KPM_EINVAL
     with pkg.KpmContext() as ctx:
         ctx.set_matrix(rp2, col2, val2, a, b)  # unchecked by default
+
+
+def test_c3_full_m_r16(pkg):
+    """C3 at M = 2000 with the R = 16 default (the bench's by_R entry; 8-lane block-cache map,
+    library order): columns 0 and 15 element by element against the oracle."""
+    lat, rp, col, val, a, b = problem((200, 100, 40))
+    M, R = 2000, 16
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments(M, R, SEED)
+        assert ctx.last_kernel() == pkg.variant_name(R, 0)
+    assert mu[0] == lat.n
+    threads = oracle.max_threads()
+    for c in (0, 15):
+        eta_o = oracle.kpm_eta(rp, col, val, a, b, M, 1, SEED, col_begin=c, threads=threads)
+        check(eta[c : c + 1], None, eta_o, cols=[0])
 
 
 def test_bench_config_c3_full_m(pkg):
