@@ -21,6 +21,9 @@
  *   - On an error the context stays usable, except after KPM_ECUDA / KPM_ENCCL, after
  *     which only kpm_destroy and kpm_last_error are valid.
  *   - One host thread per context at a time.
+ *   - nranks > 1 (NCCL): kpm_moments* and the setup collectives poll NCCL's asynchronous error
+ *     state while they wait for the device; an error NCCL reports aborts the communicator and
+ *     returns KPM_ENCCL.  A peer that dies silently is not detected (no watchdog).
  *   - nranks > 1: kpm_create, kpm_set_matrix and kpm_moments* are collective: every rank
  *     calls them in the same order with identical n_global, a, b, M, R, seed; the row
  *     ranges [row_begin, row_end) tile [0, n_global) in rank order (the data-parallel

@@ -16,9 +16,11 @@
 #include <nccl.h>
 
 #include <array>
+#include <chrono>
 #include <condition_variable>
 #include <map>
 #include <mutex>
+#include <thread>
 
 #include "../../include/kpm.h"
 #include "chunk_order.h"
@@ -356,9 +358,12 @@ extern "C" kpm_status kpm_get_unique_id(void* out) {
   return KPM_OK;
 }
 
+static kpm_status wait_stream(kpm_ctx* ctx, cudaStream_t str);
+
 // Small host<->device collective helpers for the setup (synchronous, compute stream).
 static kpm_status allgather_i64(kpm_ctx* ctx, const std::vector<int64_t>& mine, std::vector<int64_t>& all) {
   const size_t n = mine.size(), P = (size_t)ctx->opt.nranks;
+  KPM_TRACE_LINE(ctx->opt.rank, "allgather of %zu words", n);
   if (ctx->vg) {
     all.clear();
     for (const auto& v : ctx->vg->allgatherv(ctx->opt.rank, mine)) all.insert(all.end(), v.begin(), v.end());
@@ -370,7 +375,8 @@ static kpm_status allgather_i64(kpm_ctx* ctx, const std::vector<int64_t>& mine, 
   KPM_NCCL(ncclAllGather(d, d + n, n, ncclInt64, ctx->comm, ctx->stream));
   all.resize(n * P);
   KPM_CUDA(cudaMemcpyAsync(all.data(), d + n, sizeof(int64_t) * n * P, cudaMemcpyDeviceToHost, ctx->stream));
-  KPM_CUDA(cudaStreamSynchronize(ctx->stream));
+  const kpm_status ws = wait_stream(ctx, ctx->stream);
+  if (ws != KPM_OK) return ws;
   KPM_CUDA(cudaFree(d));
   return KPM_OK;
 }
@@ -1023,6 +1029,32 @@ static kpm_status plan_tiled_feed(kpm_ctx* ctx, int Rk, bool with_w, int pref_st
   return KPM_OK;
 }
 
+// Failure detection: wait for the compute stream of a multi-rank call while polling
+// NCCL's asynchronous error state; an error NCCL reports aborts the communicator and leaves the
+// context sticky (KPM_ENCCL) instead of waiting forever.  (A peer that dies silently is not
+// detected: a blocked NCCL host call or a halo-flag wait would need a watchdog thread and device
+// progress counters -- DESIGN.md §11.)  Single rank: a plain synchronize.
+static kpm_status wait_stream(kpm_ctx* ctx, cudaStream_t str) {
+  if (!ctx->comm) {
+    KPM_CUDA(cudaStreamSynchronize(str));
+    return KPM_OK;
+  }
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(str);
+    if (q == cudaSuccess) return KPM_OK;
+    if (q != cudaErrorNotReady) KPM_CUDA(q);
+    ncclResult_t ar = ncclSuccess;
+    if (ncclCommGetAsyncError(ctx->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+      KPM_TRACE_LINE(ctx->opt.rank, "wait_stream: NCCL async error %d, aborting", (int)ar);
+      ncclCommAbort(ctx->comm);
+      ctx->comm = nullptr;
+      ctx->sticky = true;
+      return fail(ctx, KPM_ENCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(ar));
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
 // Block-cache plan (per-position copy records, tile maps, absolute tile rows) of variant v for
 // this grid and chunk order, built once and cached under bc_key.  ok = every tile fits.
 static kpm_status build_bc_plan(kpm_ctx* ctx, int Rk, int v, const TileLayout& tl, int grid, bool& ok) {
@@ -1390,7 +1422,7 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   KPM_CUDA(cudaMemcpyAsync(ctx->h_eta + ctx->eta_cap, ctx->eta_odd, sizeof(double2) * n_sweeps * Rk,
                            cudaMemcpyDeviceToHost, str));
   if (last) KPM_CUDA(cudaEventRecord(ctx->ev[3], str));
-  KPM_CUDA(cudaStreamSynchronize(str));
+  if ((st = wait_stream(ctx, str)) != KPM_OK) return st;
   for (int r = 0; r < rb; ++r)
     for (int m = 0; m < n_sweeps; ++m) {
       eta_cols[(size_t)r * M + 2 * m] = ctx->h_eta[(size_t)m * Rk + r];

@@ -45,3 +45,4 @@ def test_multi_gpu_full_size_c4_bloch(world):
     assert res.returncode == 0 and lines, res.stdout[-3000:] + res.stderr[-3000:]
     out = json.loads(lines[-1][len("MGPU_BLOCH "):])
     assert out["world"] == world and out["ok"], out
+
