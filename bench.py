@@ -106,7 +106,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-def cache_roofline(n_loc, nnz_loc, R, sm_mhz, sweep_ms, hbm_gbs, wavefronts):
+def cache_roofline(n_loc, nnz_loc, R, sm_mhz, sweep_ms, hbm_gbs, wavefronts, sms=148):
     """The shared-memory ceiling of the sweep, independent of the kernel's own instruction count:
     the method needs at least every stored nonzero's V row (16 R bytes) delivered to registers
     (the row is gathered once per nonzero), and the SM's shared-memory data path
@@ -116,7 +116,6 @@ def cache_roofline(n_loc, nnz_loc, R, sm_mhz, sweep_ms, hbm_gbs, wavefronts):
     if not os.path.exists(p) or not sm_mhz:
         return None
     peak = float(json.load(open(p))["peak_lds128_B_per_clk_per_sm"])
-    sms = 148
     min_bytes = nnz_loc * 16.0 * R
     t_smem = min_bytes / (sms * peak * sm_mhz * 1e6) * 1e3
     t_hbm = alg_bytes_per_sweep(n_loc, nnz_loc, R) / (hbm_gbs * 1e9) * 1e3
@@ -425,7 +424,7 @@ def main():
         "gpu_launches": args.steps * n_blocks * ((M // 2) * (2 if world > 1 else 1) + 2),
         "clocks": clocks,
     }
-    out["cache_roofline"] = cache_roofline(n_loc, nnz_loc, R, clocks.get("sm_mhz"), sweep, hbm, smem_wf)
+    out["cache_roofline"] = cache_roofline(n_loc, nnz_loc, R, clocks.get("sm_mhz"), sweep, hbm, smem_wf, sms)
     # R sweep of the same lattice (HBM -> cache bottleneck shift), shorter M
     if not args.no_r_sweep and world == 1:
         by_r = {}
