@@ -560,7 +560,8 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
 #pragma unroll
         for (int cc = 0; cc < CPL; ++cc) u[cc] = make_double2(0.0, 0.0);
         const double2* sv = sval + kr;
-        const uint16_t* sl = slc + kr;
+        const int lts = BC ? tl.lt_stride : 0;  // row-major tile indices (TileLayout::lt_stride)
+        const uint16_t* sl = lts ? slc + kr * lts : slc + kr;
         const double2* sVt = sV + t;
         int j = 0;
         // The SELL order puts a row's own-position (diagonal) entry first, if stored (DESIGN.md
@@ -574,7 +575,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
         int li0 = -1;
         if (L > 0) {  // uniform per tile
           const double2 h0 = sv[0];
-          li0 = sl[0] * R;
+          li0 = (lts ? sl[lts - 4] : sl[0]) * R;
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) {
             x0[cc] = sVt[li0 + (cc ^ sw) * LPR];
@@ -587,9 +588,16 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
           double2 h[U];
           int li[U];
 #pragma unroll
-          for (int uu = 0; uu < U; ++uu) {
-            h[uu] = sv[(j + uu) * kC];
-            li[uu] = sl[(j + uu) * kC] * R;
+          for (int uu = 0; uu < U; ++uu) h[uu] = sv[(j + uu) * kC];
+          if (U == 4 && lts && ((j - 1) & 3) == 0) {  // one 8-byte load: entries j..j+3
+            const uint2 q4 = *reinterpret_cast<const uint2*>(sl + (j - 1));
+            li[0] = (int)(q4.x & 0xFFFFu) * R;
+            li[1 % U] = (int)(q4.x >> 16) * R;
+            li[2 % U] = (int)(q4.y & 0xFFFFu) * R;
+            li[3 % U] = (int)(q4.y >> 16) * R;
+          } else {
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) li[uu] = (lts ? sl[j + uu - 1] : sl[(j + uu) * kC]) * R;
           }
           double2 x[U][CPL];
 #pragma unroll
@@ -603,7 +611,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
         }
         for (; j < L; ++j) {
           const double2 h = sv[j * kC];
-          const int li = sl[j * kC] * R;
+          const int li = (lts ? sl[j - 1] : sl[j * kC]) * R;
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h, sVt[li + (cc ^ sw) * LPR]);
         }
@@ -891,14 +899,15 @@ TileLayout plan_tiles(int R, int64_t max_other, int64_t max_width, int stages, b
 // pool takes the rest of the budget in 32-row blocks: at least 5 S, so that S tiles without
 // any reuse (TI: own + 4 neighbour blocks each) can be in flight.
 constexpr int kBcExtraRows = 8;
-TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas) {
+TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas, bool lcol_t) {
   TileLayout tl;
   const int64_t rowb = 16ll * R;
   const int S = stages > 0 ? stages : 2;
   auto up = [&](int64_t b) { return (b + rowb - 1) / rowb * rowb; };
   const int64_t extra = kBcExtraRows * rowb;
   const int64_t w = with_w ? kC * rowb : 0;
-  const int64_t val = round128(kC * max_width * 16), lc = round128(kC * max_width * 2);
+  const int64_t lt = lcol_t ? ((std::max<int64_t>(max_width, 1) - 1 + 3) / 4) * 4 + 4 : 0;
+  const int64_t val = round128(kC * max_width * 16), lc = round128(kC * (lcol_t ? lt : max_width) * 2);
   const int64_t stage = up(extra + w + val + lc);
   const int64_t pool = kTileBudget / std::max(ctas, 1) - (ctas > 1 ? 4096 : 0) - S * stage;
   const int P = (int)std::min<int64_t>(kBcMaxSlots, pool / (kC * rowb));
@@ -911,6 +920,7 @@ TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int 
   tl.pool_slots = P;
   tl.pool_bytes = (int)(P * kC * rowb);
   tl.extra_rows = kBcExtraRows;
+  tl.lt_stride = (int)lt;
   return tl;
 }
 

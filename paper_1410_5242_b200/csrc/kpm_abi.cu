@@ -168,6 +168,7 @@ struct kpm_ctx {
   int64_t chosen_gen[6] = {-1, -1, -1, -1, -1, -1};  // ... for this matrix_gen ...
   int chosen_ovr[6] = {-2, -2, -2, -2, -2, -2};      // ... and this KPM_VARIANT override
   bool bc_ok = false;
+  bool lcol_t = false;             // block-cache feed: row-major tile indices (env KPM_LCOL_T)
   double last_total_ms = 0.0, last_sweep_ms = 0.0;
   int last_n_sweeps = 0;
   std::vector<cudaEvent_t> sweep_ev;   // KPM_TIMING: one event after every sweep of a block
@@ -293,6 +294,7 @@ extern "C" kpm_status kpm_create(kpm_ctx** out, const kpm_options* opt) {
   ctx->grid_per_sm = std::max(0, env_int("KPM_GRID_PER_SM", 0));
   ctx->tile_stages = std::max(0, env_int("KPM_TILE_STAGES", 0));
   ctx->use_graph = env_int("KPM_GRAPH", 1) != 0;
+  ctx->lcol_t = env_int("KPM_LCOL_T", 1) != 0;
   *out = ctx;
   return KPM_OK;
 }
@@ -1060,7 +1062,8 @@ static kpm_status wait_stream(kpm_ctx* ctx, cudaStream_t str) {
 static kpm_status build_bc_plan(kpm_ctx* ctx, int Rk, int v, const TileLayout& tl, int grid, bool& ok) {
   const DevSell& s = ctx->sell;
   const bool wst = variant_wstage(Rk, v);
-  const std::vector<int64_t> key = {Rk, grid, ctx->matrix_gen, ctx->order_gen, tl.stages, wst ? 1 : 0, tl.pool_slots};
+  const std::vector<int64_t> key = {Rk, grid, ctx->matrix_gen, ctx->order_gen, tl.stages, wst ? 1 : 0, tl.pool_slots,
+                                    tl.lt_stride};
   if (key == ctx->bc_key) {
     ok = ctx->bc_ok;
     return KPM_OK;
@@ -1071,7 +1074,8 @@ static kpm_status build_bc_plan(kpm_ctx* ctx, int Rk, int v, const TileLayout& t
       (ctx->opt.nranks == 1 ||
        reserve((void**)&ctx->bc_rec2, &ctx->bc_rec2_cap, sizeof(uint4) * kRecSlots * s.n_chunks) == cudaSuccess) &&
       reserve((void**)&ctx->bc_map, &ctx->bc_map_cap, sizeof(int) * kBcMapInts * s.n_chunks) == cudaSuccess &&
-      reserve((void**)&ctx->bc_lcol, &ctx->bc_lcol_cap, sizeof(uint16_t) * s.n_slots) == cudaSuccess &&
+      reserve((void**)&ctx->bc_lcol, &ctx->bc_lcol_cap,
+              sizeof(uint16_t) * std::max<int64_t>(s.n_slots, s.n_chunks * kC * (int64_t)tl.lt_stride)) == cudaSuccess &&
       reserve((void**)&ctx->bc_fail, &ctx->bc_fail_cap, sizeof(int)) == cudaSuccess;
   if (!mem_ok) {  // no room for the plan: another variant runs
     cudaGetLastError();
@@ -1124,7 +1128,8 @@ static kpm_status select_variant(kpm_ctx* ctx, int Rk, int& variant, TileLayout&
     const int bcc = variant_bc(Rk, v);
     kpm_status st;
     if (bcc) {
-      pl = s.tiles_ok ? plan_tiles_bc(Rk, s.max_width, variant_wstage(Rk, v), variant_stages(Rk, v), bcc)
+      pl = s.tiles_ok ? plan_tiles_bc(Rk, s.max_width, variant_wstage(Rk, v), variant_stages(Rk, v), bcc,
+                                      ctx->lcol_t)
                       : TileLayout();
       ok = pl.stages >= 1;
     } else if (variant_tiled(Rk, v)) {

@@ -60,6 +60,10 @@ struct TileLayout {
   // 32 V rows][stage 0]..[stage S-1]; a stage holds [extra_rows V rows | W | val | lcol] and
   // starts at pool_bytes + s * stage_bytes; all offsets are multiples of one V row (16 R bytes)
   int pool_bytes = 0, pool_slots = 0, extra_rows = 0;
+  // block-cache feed with row-major tile indices (lt_stride > 0): in a chunk's lcol block row k's
+  // entries 1..L-1 sit at k*lt_stride + 0..L-2 (padded to a multiple of 4) and entry 0 at
+  // k*lt_stride + lt_stride - 4, so one 8-byte load gives a batch of 4 entries (kernels.cu)
+  int lt_stride = 0;
 };
 constexpr int kBcMaxSlots = 16;  // block-cache pool slots (max)
 constexpr int kBcMapInts = 40;   // per tile: [n_blocks, (block, smem row) x 7, -, n_extra, (row, count, smem row) x 8]
@@ -166,7 +170,7 @@ cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* ru
                             const int64_t* list, int64_t n_chunks, int grid, int R, bool with_w,
                             const TileLayout& tl, uint4* rec, int* map, uint16_t* lcol_bc, int* fail,
                             cudaStream_t s);
-TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas);
+TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas, bool lcol_t = false);
 int variant_bc(int R, int variant);  // block-cache feed: CTAs per SM it is planned for, 0 = other feed
 int base_variant(int R);             // first variant of width R that is not a block-cache feed
 int variant_strip(int R, int variant);  // width (1, 2) of the library's line walk for this variant

@@ -380,7 +380,10 @@ __global__ void bc_plan_kernel(const int64_t* __restrict__ cptr, const int* __re
     }
     if (nslot) {
       cmd(2, s0 * 16, stage + tl.off_val, nslot * 16);
-      cmd(3, s0 * 2, stage + tl.off_lcol, nslot * 2);
+      if (tl.lt_stride)  // row-major tile indices: fixed-size block per chunk
+        cmd(3, c * kC * tl.lt_stride * 2, stage + tl.off_lcol, (int64_t)kC * tl.lt_stride * 2);
+      else
+        cmd(3, s0 * 2, stage + tl.off_lcol, nslot * 2);
     }
     for (int q = n + 1; q < kRecSlots; ++q) r[q] = make_uint4(0u, 0u, 0u, 0u);
     r[0] = make_uint4((uint32_t)total, (uint32_t)(total - wbytes), (uint32_t)(nslot / kC),
@@ -392,7 +395,7 @@ __global__ void bc_plan_kernel(const int64_t* __restrict__ cptr, const int* __re
 // Tile-row index (absolute shared-memory V row) of every SELL slot, one warp per tile.
 __global__ void bc_lcol_kernel(const int* __restrict__ scol, const int64_t* __restrict__ cptr,
                                const int64_t* __restrict__ list, int64_t n_chunks, const int* __restrict__ map,
-                               uint16_t* __restrict__ lcol, int* __restrict__ fail) {
+                               uint16_t* __restrict__ lcol, int* __restrict__ fail, int lts) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t pos = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); pos < n_chunks; pos += warps) {
@@ -407,7 +410,13 @@ __global__ void bc_lcol_kernel(const int* __restrict__ scol, const int64_t* __re
       for (int i = 0; i < nx && row < 0; ++i)
         if (g >= m[16 + 3 * i] && g < m[16 + 3 * i] + m[17 + 3 * i]) row = m[18 + 3 * i] + g - m[16 + 3 * i];
       if (row < 0 || row > 65535) atomicOr(fail, 2);
-      lcol[e] = (uint16_t)max(row, 0);
+      if (lts) {  // row-major: entries 1.. at k*lts + j - 1, entry 0 at k*lts + lts - 4
+        const int64_t off = e - cptr[c];
+        const int j = (int)(off / kC), k = (int)(off % kC);
+        lcol[(c * kC + k) * lts + (j == 0 ? lts - 4 : j - 1)] = (uint16_t)max(row, 0);
+      } else {
+        lcol[e] = (uint16_t)max(row, 0);
+      }
     }
   }
 }
@@ -425,7 +434,8 @@ cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* ru
                             cudaStream_t s) {
   bc_plan_kernel<<<(grid + 63) / 64, 64, 0, s>>>(cptr, nruns, runs, list, n_chunks, grid, R, with_w ? 1 : 0, tl, rec,
                                                   map, fail);
-  bc_lcol_kernel<<<grid_for(n_chunks * 32, 256), 256, 0, s>>>(scol, cptr, list, n_chunks, map, lcol_bc, fail);
+  bc_lcol_kernel<<<grid_for(n_chunks * 32, 256), 256, 0, s>>>(scol, cptr, list, n_chunks, map, lcol_bc, fail,
+                                                               tl.lt_stride);
   return cudaGetLastError();
 }
 
