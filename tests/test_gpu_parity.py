@@ -369,6 +369,48 @@ def test_block_cache_feed(pkg, monkeypatch, ordered, R, dims, name, ctas):
     check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, M, R, SEED))
 
 
+def _full_orbital_blocks(dims, seed=5):
+    """The TI plus random complex Hermitian couplings filling its on-site and +-x 4x4 orbital
+    blocks: the same 32-row block neighbourhoods as the
+    TI, so the block-cache plan fits, but rows of 18-20 entries (4-entry batches plus remainders,
+    wider val / lcol blocks per stage) instead of the TI's 11-13."""
+    import scipy.sparse as sp
+
+    lat, rp, col, val, _, _ = problem(dims)
+    rows = np.repeat(np.arange(lat.n), np.diff(rp))
+    sites = np.unique(np.stack([rows // 4, col // 4], 1), axis=0)
+    ns, nx_stride = lat.n // 4, dims[1] * dims[2]  # x is the slowest site index (DESIGN.md R15)
+    d = (sites[:, 1] - sites[:, 0]) % ns
+    sites = sites[(d == 0) | (d == nx_stride) | (d == ns - nx_stride)]  # own and +-x blocks filled
+    o = np.arange(4)
+    r = (sites[:, :1, None] * 4 + o[None, :, None] + 0 * o[None, None, :]).reshape(-1)
+    c = (sites[:, 1:, None] * 4 + 0 * o[None, :, None] + o[None, None, :]).reshape(-1)
+    rng = np.random.default_rng(seed)
+    z = rng.normal(size=len(r)) + 1j * rng.normal(size=len(r))
+    h = sp.coo_matrix((z, (r, c)), shape=(lat.n, lat.n)).tocsr()
+    h = (h + h.conj().T + sp.csr_matrix((val, col, rp), shape=(lat.n, lat.n))).tocsr()
+    h.sort_indices()
+    rp2, col2, val2 = h.indptr.astype(np.int64), h.indices.astype(np.int64), h.data.astype(np.complex128)
+    a, b = scale_factors(*gershgorin(rp2, col2, val2))
+    return lat, rp2, col2, val2, a, b
+
+
+@pytest.mark.parametrize("R,name", [(32, "tiled.bc.lpr8.u4"), (16, "tiled.bc.lpr8.u4.wr")])
+def test_block_cache_wide_rows(pkg, monkeypatch, R, name):
+    """Rows of 18-20 entries on the block-cache feed (the R = 16 / 32 defaults): oracle-exact, and
+    the named variant really ran (its shared-memory plan still fits)."""
+    lat, rp, col, val, a, b = _full_orbital_blocks((24, 10, 32))
+    assert np.diff(rp).max() > 16
+    idx = [pkg.variant_name(R, v) for v in range(16)].index(name)
+    monkeypatch.setenv("KPM_VARIANT", str(idx))
+    M = 24
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, val, a, b)
+        mu, eta = ctx.moments(M, R, SEED)
+        assert ctx.last_kernel() == name
+    check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, M, R, SEED))
+
+
 @pytest.mark.parametrize("R", [1, 8, 32])
 def test_irregular_matrix_fallback(pkg, R):
     """A random Hermitian matrix with empty rows, wide rows (up to ~200 entries) and scattered
