@@ -344,6 +344,7 @@ def test_rows_without_diagonal(pkg, R):
 
 @pytest.mark.parametrize("ordered", [False, True])
 @pytest.mark.parametrize("R,dims,name,ctas", [(32, (40, 20, 32), "tiled.bc.lpr8.u4", 1),
+                                             (32, (40, 20, 32), "tiled.bc.quad", 1),
                                              (16, (80, 12, 32), "tiled.bc.lpr8.u4.wr", 2),
                                              (16, (80, 12, 32), "tiled.bc.lpr4.u4.wr", 2),
                                              (8, (120, 8, 32), "tiled.bc.lpr4.u4.wr", 3)])
@@ -395,7 +396,7 @@ def _full_orbital_blocks(dims, seed=5):
     return lat, rp2, col2, val2, a, b
 
 
-@pytest.mark.parametrize("R,name", [(32, "tiled.bc.lpr8.u4"), (16, "tiled.bc.lpr8.u4.wr")])
+@pytest.mark.parametrize("R,name", [(32, "tiled.bc.lpr8.u4"), (32, "tiled.bc.quad"), (16, "tiled.bc.lpr8.u4.wr")])
 def test_block_cache_wide_rows(pkg, monkeypatch, R, name):
     """Rows of 18-20 entries on the block-cache feed (the R = 16 / 32 defaults): oracle-exact, and
     the named variant really ran (its shared-memory plan still fits)."""
