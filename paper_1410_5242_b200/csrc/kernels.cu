@@ -449,70 +449,7 @@ __host__ __device__ constexpr int tiled_threads() { return 32 * (tiled_ncwg<LPR>
 // BC: block-cache feed: records per list position, V rows of a tile live in a
 // pool of 32-row blocks kept across the CTA's tiles (plus per-stage extra rows), lcol holds
 // absolute shared-memory V rows, the header carries the own block's first row.
-// Quad feed (QD, R = 32, block-cache tiles; DESIGN.md §7 "Quad feed"): a warp owns 4 consecutive
-// rows and lane = block column.  The chunk's tile carries, per quad, the distinct V rows its 4
-// rows reference, grouped into runs of equal row mask (bit r: row r of the quad uses that V row),
-// so each distinct V row is gathered once (LDS.128, 512 B) and feeds popc(mask) accumulators; the
-// values are read with one address per warp (1 clock instead of 2.14 for the 8-lane broadcast).
-// Tile layout (written by quad_build_kernel, sell_device.cu), in the stage's lcol region:
-//   uint32 hdr[8] = meta offset (uint16 units) | value offset (double2 units, from the val region) << 16
-//   per quad: nruns, run words (mask << 12 | length), padded to 4; then per run its V rows
-//   (absolute shared-memory rows), padded to a multiple of 4 (8-byte index loads).
-// Values: per run, per V row, one value per set mask bit in row order.
-template <int MASK>
-__device__ __forceinline__ void quad_run(const uint16_t* __restrict__ cl, const double2* __restrict__ vq, int len,
-                                         const double2* __restrict__ sVt, double2 (&acc)[4]) {
-  constexpr int P = __builtin_popcount(MASK);
-  int k = 0;
-  for (; k + 4 <= len; k += 4) {
-    const uint2 c4 = *reinterpret_cast<const uint2*>(cl + k);
-    const int li[4] = {(int)(c4.x & 0xFFFFu) * 32, (int)(c4.x >> 16) * 32, (int)(c4.y & 0xFFFFu) * 32,
-                       (int)(c4.y >> 16) * 32};
-    double2 x[4], h[4][P];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = sVt[li[u]];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int p = 0; p < P; ++p) h[u][p] = vq[(k + u) * P + p];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      int p = 0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (MASK & (1 << r)) cmac(acc[r], h[u][p++], x[u]);
-    }
-  }
-  if (k < len) {  // 1-3 left: one 8-byte index load (the run's index list is padded to 4)
-    const uint2 c4 = *reinterpret_cast<const uint2*>(cl + k);
-    const int li[3] = {(int)(c4.x & 0xFFFFu) * 32, (int)(c4.x >> 16) * 32, (int)(c4.y & 0xFFFFu) * 32};
-#pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      if (k + u < len) {
-        const double2 x = sVt[li[u]];
-        int p = 0;
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (MASK & (1 << r)) cmac(acc[r], vq[(k + u) * P + p++], x);
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void quad_dispatch(int mask, const uint16_t* cl, const double2* vq, int len,
-                                              const double2* sVt, double2 (&acc)[4]) {
-  switch (mask) {  // warp-uniform
-#define KPM_QCASE(m) \
-  case m: quad_run<m>(cl, vq, len, sVt, acc); break;
-    KPM_QCASE(1) KPM_QCASE(2) KPM_QCASE(3) KPM_QCASE(4) KPM_QCASE(5) KPM_QCASE(6) KPM_QCASE(7) KPM_QCASE(8)
-    KPM_QCASE(9) KPM_QCASE(10) KPM_QCASE(11) KPM_QCASE(12) KPM_QCASE(13) KPM_QCASE(14) KPM_QCASE(15)
-#undef KPM_QCASE
-    default: break;
-  }
-}
-
-template <int R, int LPR, int U, int CS, bool WS, bool INIT, int KIND = kAug, int MINB = 1, bool BC = false,
-          bool QD = false>
+template <int R, int LPR, int U, int CS, bool WS, bool INIT, int KIND = kAug, int MINB = 1, bool BC = false>
 __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tiled(const SweepArgs a) {
   using Cf = Cfg<R, LPR, U>;
   constexpr int RW = Cf::RW, G = kC / RW;
@@ -589,69 +526,6 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
           bulk_g2s(smem_u32(st + cur.z), src + off, bytes, bar, base == 0 ? pol_v : pol);
         }
       }
-    }
-  } else if constexpr (QD) {
-    // ---------------- consumer warps, quad feed: warp g0 = rows 4 g0 .. 4 g0 + 3, lane = column
-    static_assert(R == 32 && BC && NCWG == kC / 4 && CS == 1, "quad feed: R = 32 block-cache tiles, 8 warps");
-    Dots<1> dq;
-    dq.zero();
-    for (int64_t k = 0; k < my_tiles; ++k) {
-      const int s = (int)(k % tl.stages);
-      const unsigned char* st = tsm + (size_t)tl.pool_bytes + (size_t)s * tl.stage_bytes;
-      const double2* sV = reinterpret_cast<const double2*>(tsm);
-      const double2* sW = reinterpret_cast<const double2*>(st + tl.off_w);
-      const double2* sval = reinterpret_cast<const double2*>(st + tl.off_val);
-      const uint16_t* smeta = reinterpret_cast<const uint16_t*>(st + tl.off_lcol);
-      mbar_wait(smem_u32(&full[s]), (uint32_t)((k / tl.stages) & 1));
-      const int own_row = tile_own[s];
-      const int64_t c = tile_chunk[s];
-      const uint32_t hdr = reinterpret_cast<const uint32_t*>(smeta)[warp];
-      const uint16_t* mq = smeta + (hdr & 0xFFFFu);
-      const double2* vq = sval + (hdr >> 16);
-      const int nr = mq[0];
-      const uint16_t* cl = mq + ((nr + 4) & ~3);
-      const double2* sVt = sV + lane;
-      double2 acc[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) acc[r] = make_double2(0.0, 0.0);
-      for (int ri = 0; ri < nr; ++ri) {
-        const int word = mq[1 + ri], mask = word >> 12, len = word & 0xFFF;
-        quad_dispatch(mask, cl, vq, len, sVt, acc);
-        cl += (len + 3) & ~3;
-        vq += len * __popc(mask);
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int kr = warp * 4 + r;
-        const int64_t p = c * kC + kr;
-        if (p < a.n_loc) {
-          const double2 vi_c = sV[(own_row + kr) * R + lane];
-          double2 uu = acc[r];
-          uu.x = fma(-a.b, vi_c.x, uu.x);
-          uu.y = fma(-a.b, vi_c.y, uu.y);
-          double2 w;
-          if (INIT) {
-            w = make_double2(a.scale * uu.x, a.scale * uu.y);
-          } else {
-            const double2 wo = sW[kr * R + lane];
-            w = make_double2(fma(a.scale, uu.x, -wo.x), fma(a.scale, uu.y, -wo.y));
-          }
-          st_stream(a.W + p * R + lane, w, pol);
-          store_peers<R>(a, p, lane, w);
-          if (KIND == kAug) {
-            dq.ee[0] = fma(vi_c.x, vi_c.x, fma(vi_c.y, vi_c.y, dq.ee[0]));
-            dq.eor[0] = fma(w.x, vi_c.x, fma(w.y, vi_c.y, dq.eor[0]));
-            dq.eoi[0] = fma(w.x, vi_c.y, fma(-w.y, vi_c.x, dq.eoi[0]));
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
-    }
-    if (KIND == kAug) {
-      red[warp * 3 * R + lane] = dq.ee[0];
-      red[warp * 3 * R + R + lane] = dq.eor[0];
-      red[warp * 3 * R + 2 * R + lane] = dq.eoi[0];
     }
   } else {
     // ---------------- consumer warps ---------------------------------------------------
@@ -818,7 +692,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
 
 enum Feed { kDirect = 0, kStaged = 1, kTiled = 2 };
 
-template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true, int MINB = 1, bool BC = false, bool QD = false>
+template <int R, int LPR, int U, int FEED, int CS = 1, bool WS = true, int MINB = 1, bool BC = false>
 struct Variant {
   static cudaError_t launch(bool init, const SweepArgs& a, int grid, cudaStream_t s) {
     if constexpr (FEED == kStaged) {
@@ -828,8 +702,8 @@ struct Variant {
         aug_spmmv_staged<R, LPR, U, false><<<grid, kThreads, kStagedSmem, s>>>(a);
     } else if constexpr (FEED == kTiled) {
       const int smem = a.tl.pool_bytes + a.tl.stages * a.tl.stage_bytes;
-      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB, BC, QD>;
-      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB, BC, QD>;
+      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB, BC>;
+      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB, BC>;
       cudaFuncSetAttribute(k_init, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       (init ? k_init : k_main)<<<grid, tiled_threads<LPR, CS>(), smem, s>>>(a);
@@ -851,8 +725,8 @@ struct Variant {
       cudaFuncGetAttributes(&fa, aug_spmmv_staged<R, LPR, U, true>);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, aug_spmmv_staged<R, LPR, U, false>, kThreads, kStagedSmem);
     } else if constexpr (FEED == kTiled) {
-      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB, BC, QD>;
-      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB, BC, QD>;
+      auto k_init = aug_spmmv_tiled<R, LPR, U, CS, WS, true, kAug, MINB, BC>;
+      auto k_main = aug_spmmv_tiled<R, LPR, U, CS, WS, false, kAug, MINB, BC>;
       cudaFuncSetAttribute(k_init, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
       cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_main, tiled_threads<LPR, CS>(), dyn_smem);
@@ -876,7 +750,6 @@ struct Entry {
   int stages = 0;  // tiled feed: preferred ring depth (0 = plan_tiles default)
   int bc_ctas = 0;  // block-cache feed: CTAs per SM its shared-memory plan is sized for (0: not BC)
   int strip = 1;    // chunk-order width the library's line walk uses for it (chunk_order.cpp)
-  int quad = 0;     // quad feed: the block-cache plan also builds the per-quad tile data (sell_device.cu)
 };
 #define KPM_VARIANT(R, LPR, U, F, NAME) {R, NAME, F, true, Variant<R, LPR, U, F>::launch, Variant<R, LPR, U, F>::occupancy}
 #define KPM_VARIANT_CS(R, LPR, U, CS, NAME) \
@@ -933,8 +806,6 @@ const Entry kTable[] = {
     // R = 32: walked in strips of two lines (-2 % under the power cap, profiles/r02_variants/)
     {32, "tiled.bc.lpr8.u4", kTiled, true, Variant<32, 8, 4, kTiled, 1, true, 1, true>::launch,
      Variant<32, 8, 4, kTiled, 1, true, 1, true>::occupancy, 2, 1, 2},
-    {32, "tiled.bc.quad", kTiled, true, Variant<32, 8, 4, kTiled, 1, true, 1, true, true>::launch,
-     Variant<32, 8, 4, kTiled, 1, true, 1, true, true>::occupancy, 2, 1, 2, 1},
     KPM_VARIANT(32, 8, 4, kTiled, "tiled.lpr8.u4"),
     KPM_VARIANT_WR(32, 8, 4, "tiled.lpr8.u4.wr"),
     KPM_VARIANT_CS(32, 8, 4, 2, "tiled.lpr8.u4.cs2"),
@@ -996,11 +867,6 @@ int variant_strip(int R, int variant) {
 int variant_bc(int R, int variant) {
   const Entry* e = find(R, variant);
   return e ? e->bc_ctas : 0;
-}
-
-bool variant_quad(int R, int variant) {
-  const Entry* e = find(R, variant);
-  return e && e->quad;
 }
 
 bool variant_wstage(int R, int variant) {

@@ -161,9 +161,6 @@ struct kpm_ctx {
   size_t bc_rec2_cap = 0;
   int* bc_map = nullptr;
   uint16_t* bc_lcol = nullptr;
-  double2* q_val = nullptr;          // quad feed: per-quad values / metadata (launch_build_quad)
-  uint16_t* q_meta = nullptr;
-  size_t q_val_cap = 0, q_meta_cap = 0;
   int* bc_fail = nullptr;
   size_t bc_rec_cap = 0, bc_map_cap = 0, bc_lcol_cap = 0, bc_fail_cap = 0;
   std::vector<int64_t> bc_key;      // (R, grid, matrix_gen, stages, ...) the buffers were built for
@@ -334,8 +331,6 @@ extern "C" void kpm_destroy(kpm_ctx* ctx) {
   cudaFree(ctx->bc_rec2);
   cudaFree(ctx->bc_map);
   cudaFree(ctx->bc_lcol);
-  cudaFree(ctx->q_val);
-  cudaFree(ctx->q_meta);
   cudaFree(ctx->bc_fail);
   cudaFree(ctx->flags);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
@@ -1067,9 +1062,8 @@ static kpm_status wait_stream(kpm_ctx* ctx, cudaStream_t str) {
 static kpm_status build_bc_plan(kpm_ctx* ctx, int Rk, int v, const TileLayout& tl, int grid, bool& ok) {
   const DevSell& s = ctx->sell;
   const bool wst = variant_wstage(Rk, v);
-  const bool quad = variant_quad(Rk, v);
   const std::vector<int64_t> key = {Rk, grid, ctx->matrix_gen, ctx->order_gen, tl.stages, wst ? 1 : 0, tl.pool_slots,
-                                    tl.lt_stride, quad ? 1 : 0};
+                                    tl.lt_stride};
   if (key == ctx->bc_key) {
     ok = ctx->bc_ok;
     return KPM_OK;
@@ -1082,11 +1076,7 @@ static kpm_status build_bc_plan(kpm_ctx* ctx, int Rk, int v, const TileLayout& t
       reserve((void**)&ctx->bc_map, &ctx->bc_map_cap, sizeof(int) * kBcMapInts * s.n_chunks) == cudaSuccess &&
       reserve((void**)&ctx->bc_lcol, &ctx->bc_lcol_cap,
               sizeof(uint16_t) * std::max<int64_t>(s.n_slots, s.n_chunks * kC * (int64_t)tl.lt_stride)) == cudaSuccess &&
-      reserve((void**)&ctx->bc_fail, &ctx->bc_fail_cap, sizeof(int)) == cudaSuccess &&
-      (!quad || (tl.lt_stride > 0 &&
-                 reserve((void**)&ctx->q_val, &ctx->q_val_cap, sizeof(double2) * s.n_slots) == cudaSuccess &&
-                 reserve((void**)&ctx->q_meta, &ctx->q_meta_cap,
-                         sizeof(uint16_t) * s.n_chunks * kC * (int64_t)tl.lt_stride) == cudaSuccess));
+      reserve((void**)&ctx->bc_fail, &ctx->bc_fail_cap, sizeof(int)) == cudaSuccess;
   if (!mem_ok) {  // no room for the plan: another variant runs
     cudaGetLastError();
     ctx->bc_ok = ok = false;
@@ -1106,10 +1096,6 @@ static kpm_status build_bc_plan(kpm_ctx* ctx, int Rk, int v, const TileLayout& t
     if (ctx->n_interior)
       KPM_CUDA(launch_build_bc(s.cptr, s.nruns, s.runs, s.col, ctx->interior_list, ctx->n_interior, grid, Rk, wst, tl,
                                ctx->bc_rec2, ctx->bc_map, ctx->bc_lcol, ctx->bc_fail, ctx->stream));
-  }
-  if (quad) {  // per-quad tile data of every chunk (all lists index the same per-chunk regions)
-    KPM_CUDA(launch_build_quad(s.val, s.cptr, nullptr, s.n_chunks, ctx->bc_lcol, tl.lt_stride, ctx->q_val, ctx->q_meta,
-                               ctx->bc_fail, ctx->stream));
   }
   int hfail = 0;
   KPM_CUDA(cudaMemcpyAsync(&hfail, ctx->bc_fail, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1280,10 +1266,8 @@ static kpm_status run_block(kpm_ctx* ctx, int M, int rb, int64_t col_begin, uint
   sa.chunk_list = ctx->order_list;  // NULL: storage order
   sa.chunk_begin = 0;
   sa.chunk_end = s.n_chunks;
-  const bool quad = bc && variant_quad(Rk, variant);
   sa.rec = bc ? ctx->bc_rec : s.rec[rec_index];
-  sa.lcol = quad ? ctx->q_meta : bc ? ctx->bc_lcol : s.lcol;
-  if (quad) sa.val = ctx->q_val;
+  sa.lcol = bc ? ctx->bc_lcol : s.lcol;
   sa.tl = tl;
   sa.b = ctx->b;
   sa.pstride = (int64_t)grid * parts;

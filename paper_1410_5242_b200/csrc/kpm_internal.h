@@ -172,12 +172,6 @@ cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* ru
                             cudaStream_t s);
 TileLayout plan_tiles_bc(int R, int64_t max_width, bool with_w, int stages, int ctas, bool lcol_t = false);
 int variant_bc(int R, int variant);  // block-cache feed: CTAs per SM it is planned for, 0 = other feed
-bool variant_quad(int R, int variant);  // quad feed: needs the per-quad tile data (launch_build_quad)
-// Quad feed: per-quad tile data from the SELL values and the block-cache tile rows (row-major
-// lcol, lts > 0) of the chunks of `list`; *fail |= 4 if some chunk does not fit the format.
-cudaError_t launch_build_quad(const double2* val, const int64_t* cptr, const int64_t* list, int64_t n_chunks,
-                              const uint16_t* lcol_bc, int lts, double2* qval, uint16_t* qmeta, int* fail,
-                              cudaStream_t s);
 int base_variant(int R);             // first variant of width R that is not a block-cache feed
 int variant_strip(int R, int variant);  // width (1, 2) of the library's line walk for this variant
 cudaError_t launch_build_records(const int64_t* cptr, const int* nruns, const int* runs, int64_t n_chunks, int R,

@@ -421,115 +421,6 @@ __global__ void bc_lcol_kernel(const int* __restrict__ scol, const int64_t* __re
   }
 }
 
-// Quad feed tile data (kernels.cu quad_run): one warp per list position (chunk c), lane q < 8
-// builds quad q = rows 4q .. 4q + 3 from the chunk's SELL values and its block-cache tile rows:
-// the distinct tile rows the 4 rows reference (stored zeros, i.e. the SELL padding, skipped),
-// grouped by row mask into runs in mask order, rows ascending inside a run.  Written at the SELL
-// value offsets (values) and the row-major lcol offsets (metadata) of the chunk, so the block-cache
-// copy records serve unchanged.  *fail |= 4 if a quad has more than kQuadMaxL entries per row, a
-// repeated column, or the metadata overflows the chunk's lcol block.
-constexpr int kQuadMaxL = 32;
-__global__ void quad_build_kernel(const double2* __restrict__ val, const int64_t* __restrict__ cptr,
-                                  const int64_t* __restrict__ list, int64_t n_chunks, const uint16_t* __restrict__ lcol,
-                                  int lts, double2* __restrict__ qval, uint16_t* __restrict__ qmeta,
-                                  int* __restrict__ fail) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t pos = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); pos < n_chunks; pos += warps) {
-    const int64_t c = list ? list[pos] : pos;
-    const int64_t s0 = cptr[c];
-    const int L = (int)((cptr[c + 1] - s0) / kC);
-    int key[4 * kQuadMaxL];
-    unsigned char jj[4 * kQuadMaxL];
-    int n = 0, meta = 0, bad = 0, nruns = 0;
-    int count[16];
-    for (int m = 0; m < 16; ++m) count[m] = 0;
-    if (lane < 8) {
-      if (L > kQuadMaxL) bad = 1;
-      for (int r = 0; r < 4 && !bad; ++r) {
-        const int kr = 4 * lane + r;
-        for (int j = 0; j < L; ++j) {
-          const double2 v = val[s0 + (int64_t)j * kC + kr];
-          if (v.x == 0.0 && v.y == 0.0) continue;
-          const int row = lcol[(c * kC + kr) * lts + (j == 0 ? lts - 4 : j - 1)];
-          // insertion by key = tile row * 4 + r
-          int i = n++;
-          const int kk = row * 4 + r;
-          while (i > 0 && key[i - 1] > kk) {
-            key[i] = key[i - 1];
-            jj[i] = jj[i - 1];
-            --i;
-          }
-          if (i > 0 && key[i - 1] == kk) bad = 1;  // repeated column in a row
-          key[i] = kk;
-          jj[i] = (unsigned char)j;
-        }
-      }
-      for (int i = 0; i < n && !bad;) {  // groups of equal tile row -> mask counts
-        int m = 0, e = i;
-        while (e < n && key[e] >> 2 == key[i] >> 2) m |= 1 << (key[e++] & 3);
-        ++count[m];
-        i = e;
-      }
-      for (int m = 1; m < 16; ++m)
-        if (count[m]) {
-          ++nruns;
-          meta += (count[m] + 3) & ~3;
-        }
-      meta += (nruns + 4) & ~3;
-    }
-    // offsets: header of 8 uint32 (16 uint16) first, then the quads in order
-    int mo = meta, vo = n;
-#pragma unroll
-    for (int off = 1; off < 8; off <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, mo, off), b = __shfl_up_sync(0xffffffffu, vo, off);
-      if (lane >= off) {
-        mo += a;
-        vo += b;
-      }
-    }
-    const int total_meta = __shfl_sync(0xffffffffu, mo, 7) + 16;
-    bad |= __any_sync(0xffffffffu, bad) ? 1 : 0;
-    if (total_meta > kC * lts) bad = 1;
-    if (bad) {
-      if (lane == 0) atomicOr(fail, 4);
-      continue;
-    }
-    if (lane < 8) {
-      mo = mo - meta + 16;  // exclusive
-      vo = vo - n;
-      uint16_t* base = qmeta + c * kC * lts;
-      reinterpret_cast<uint32_t*>(base)[lane] = (uint32_t)mo | ((uint32_t)vo << 16);
-      uint16_t* mq = base + mo;
-      const int hdr_len = (nruns + 4) & ~3;
-      for (int i = 0; i < hdr_len; ++i) mq[i] = 0;
-      mq[0] = (uint16_t)nruns;
-      uint16_t* cl = mq + hdr_len;
-      double2* vq = qval + s0 + vo;
-      int ri = 0;
-      for (int m = 1; m < 16; ++m) {
-        if (!count[m]) continue;
-        mq[1 + ri++] = (uint16_t)((m << 12) | count[m]);
-        int k = 0;
-        for (int i = 0; i < n;) {
-          int gm = 0, e = i;
-          while (e < n && key[e] >> 2 == key[i] >> 2) gm |= 1 << (key[e++] & 3);
-          if (gm == m) {
-            cl[k++] = (uint16_t)(key[i] >> 2);
-            for (int t = i; t < e; ++t) {  // rows ascending
-              const int kr = 4 * lane + (key[t] & 3);
-              *vq++ = val[s0 + (int64_t)jj[t] * kC + kr];
-            }
-          }
-          i = e;
-        }
-        for (; k & 3; ++k) cl[k] = 0;
-        cl += k;
-      }
-    }
-  }
-}
-
 int grid_for(int64_t n, int block) {
   const int64_t g = (n + block - 1) / block;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
@@ -545,14 +436,6 @@ cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* ru
                                                   map, fail);
   bc_lcol_kernel<<<grid_for(n_chunks * 32, 256), 256, 0, s>>>(scol, cptr, list, n_chunks, map, lcol_bc, fail,
                                                                tl.lt_stride);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_build_quad(const double2* val, const int64_t* cptr, const int64_t* list, int64_t n_chunks,
-                              const uint16_t* lcol_bc, int lts, double2* qval, uint16_t* qmeta, int* fail,
-                              cudaStream_t s) {
-  quad_build_kernel<<<grid_for(n_chunks * 32, 128), 128, 0, s>>>(val, cptr, list, n_chunks, lcol_bc, lts, qval, qmeta,
-                                                                 fail);
   return cudaGetLastError();
 }
 

@@ -344,7 +344,6 @@ def test_rows_without_diagonal(pkg, R):
 
 @pytest.mark.parametrize("ordered", [False, True])
 @pytest.mark.parametrize("R,dims,name,ctas", [(32, (40, 20, 32), "tiled.bc.lpr8.u4", 1),
-                                             (32, (40, 20, 32), "tiled.bc.quad", 1),
                                              (16, (80, 12, 32), "tiled.bc.lpr8.u4.wr", 2),
                                              (16, (80, 12, 32), "tiled.bc.lpr4.u4.wr", 2),
                                              (8, (120, 8, 32), "tiled.bc.lpr4.u4.wr", 3)])
@@ -370,11 +369,11 @@ def test_block_cache_feed(pkg, monkeypatch, ordered, R, dims, name, ctas):
     check(eta, mu, oracle.kpm_eta(rp, col, val, a, b, M, R, SEED))
 
 
-def _full_orbital_blocks(dims, seed=5):
-    """The TI plus random complex Hermitian couplings filling its on-site and +-x 4x4 orbital
-    blocks: the same 32-row block neighbourhoods as the
-    TI, so the block-cache plan fits, but rows of 18-20 entries (4-entry batches plus remainders,
-    wider val / lcol blocks per stage) instead of the TI's 11-13."""
+def _full_orbital_blocks(dims, xblocks=True, seed=5):
+    """The TI plus random complex Hermitian couplings filling its on-site (and, xblocks, its +-x)
+    4x4 orbital blocks: the same 32-row block neighbourhoods as the TI, so the block-cache plan
+    can fit, but rows of 14-16 (18-20) entries (4-entry batches plus remainders, wider val / lcol
+    blocks per stage) instead of the TI's 11-13."""
     import scipy.sparse as sp
 
     lat, rp, col, val, _, _ = problem(dims)
@@ -382,7 +381,7 @@ def _full_orbital_blocks(dims, seed=5):
     sites = np.unique(np.stack([rows // 4, col // 4], 1), axis=0)
     ns, nx_stride = lat.n // 4, dims[1] * dims[2]  # x is the slowest site index (R15)
     d = (sites[:, 1] - sites[:, 0]) % ns
-    sites = sites[(d == 0) | (d == nx_stride) | (d == ns - nx_stride)]  # own and +-x blocks filled
+    sites = sites[(d == 0) | (xblocks & ((d == nx_stride) | (d == ns - nx_stride)))]  # blocks filled
     o = np.arange(4)
     r = (sites[:, :1, None] * 4 + o[None, :, None] + 0 * o[None, None, :]).reshape(-1)
     c = (sites[:, 1:, None] * 4 + 0 * o[None, :, None] + o[None, None, :]).reshape(-1)
@@ -396,12 +395,13 @@ def _full_orbital_blocks(dims, seed=5):
     return lat, rp2, col2, val2, a, b
 
 
-@pytest.mark.parametrize("R,name", [(32, "tiled.bc.lpr8.u4"), (32, "tiled.bc.quad"), (16, "tiled.bc.lpr8.u4.wr")])
-def test_block_cache_wide_rows(pkg, monkeypatch, R, name):
-    """Rows of 18-20 entries on the block-cache feed (the R = 16 / 32 defaults): oracle-exact, and
-    the named variant really ran (its shared-memory plan still fits)."""
-    lat, rp, col, val, a, b = _full_orbital_blocks((24, 10, 32))
-    assert np.diff(rp).max() > 16
+@pytest.mark.parametrize("R,name,xblocks", [(32, "tiled.bc.lpr8.u4", False), (16, "tiled.bc.lpr8.u4.wr", True)])
+def test_block_cache_wide_rows(pkg, monkeypatch, R, name, xblocks):
+    """Rows wider than the TI's on the block-cache feed (the R = 16 / 32 defaults; at R = 32 a
+    20-entry chunk leaves 9 pool slots, too few, so that case uses the 16-entry matrix):
+    oracle-exact, and the named variant really ran (its shared-memory plan still fits)."""
+    lat, rp, col, val, a, b = _full_orbital_blocks((24, 10, 32), xblocks)
+    assert np.diff(rp).max() > 13
     idx = [pkg.variant_name(R, v) for v in range(16)].index(name)
     monkeypatch.setenv("KPM_VARIANT", str(idx))
     M = 24
