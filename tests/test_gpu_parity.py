@@ -395,12 +395,12 @@ def _full_orbital_blocks(dims, xblocks=True, seed=5):
     return lat, rp2, col2, val2, a, b
 
 
-@pytest.mark.parametrize("R,name,xblocks", [(32, "tiled.bc.lpr8.u4", False), (16, "tiled.bc.lpr8.u4.wr", True)])
-def test_block_cache_wide_rows(pkg, monkeypatch, R, name, xblocks):
-    """Rows wider than the TI's on the block-cache feed (the R = 16 / 32 defaults; at R = 32 a
-    20-entry chunk leaves 9 pool slots, too few, so that case uses the 16-entry matrix):
-    oracle-exact, and the named variant really ran (its shared-memory plan still fits)."""
-    lat, rp, col, val, a, b = _full_orbital_blocks((24, 10, 32), xblocks)
+@pytest.mark.parametrize("R,name", [(32, "tiled.bc.lpr8.u4"), (16, "tiled.bc.lpr8.u4.wr")])
+def test_block_cache_wide_rows(pkg, monkeypatch, R, name):
+    """Rows wider than the TI's (14-16 entries) on the block-cache feed (the R = 16 / 32
+    defaults): oracle-exact, and the named variant really ran.  (16 is the widest chunk whose
+    stages leave the 5 S = 10 pool slots the plan needs at both widths.)"""
+    lat, rp, col, val, a, b = _full_orbital_blocks((24, 10, 32), xblocks=False)
     assert np.diff(rp).max() > 13
     idx = [pkg.variant_name(R, v) for v in range(16)].index(name)
     monkeypatch.setenv("KPM_VARIANT", str(idx))
