@@ -45,8 +45,6 @@ def main():
                 from workloads.ti_lattice import chunk_order_ylines
                 sms = torch.cuda.get_device_properties(0).multi_processor_count
                 ctas = {16: 2, 32: 1}.get(R)  # default block-cache feed CTAs per SM (kernels.cu)
-                if args.variant.startswith("pair"):
-                    ctas = 1
                 ctx.set_chunk_order(chunk_order_ylines(lat, sms * ctas) if ctas else None)
             for _ in range(args.reps):
                 mu, _ = ctx.moments(args.M, R, SEED, want_eta=False)
