@@ -192,8 +192,12 @@ def workload(args, world):
 
 def config_dict(w, world):
     """config of the JSON line -- identical on both arms (driver's same_config check)."""
+    rows = 4 * w["px"] * w["ny"] * w["nz"]  # per GPU
+    ws = 32 * w["R"] * rows + 20 * 13 * rows  # V + W + matrix bytes per GPU
     return {"workload": w["name"], "lattice": [w["nx"], w["ny"], w["nz"]], "M": w["M"], "R": w["R"],
-            "parallelism": f"x-slab dp{world}"}
+            "parallelism": f"x-slab dp{world}",
+            "l2": "no flush: inputs larger than L2 (%.2f GB per GPU)" % (ws / 1e9) if ws > 126e6 else
+                  "no flush: L2-resident working set (%.0f MB per GPU)" % (ws / 1e6)}
 
 
 def host_copy_gbs(threads):

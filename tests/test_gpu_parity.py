@@ -712,3 +712,31 @@ def test_degenerate_sizes(pkg, R):
             eta_o = oracle.kpm_eta(rp, col, val, a, b, M, R, SEED)
             check(eta, mu, eta_o)
             assert mu[0] == len(rp) - 1
+
+
+@pytest.mark.parametrize("R", [1, 8, 32])
+def test_closed_forms_without_oracle(pkg, R):
+    """Pins of the CUDA path that need no oracle (mu_n = <v|T_n(H~)|v> averaged over
+    unit-modulus v): a diagonal H has mu_n = sum_i T_n(a (lambda_i - b)) exactly for every Z4
+    column, on a ragged multi-chunk size with the width's default kernel; an H with no stored
+    entry at all (every chunk empty) is H~ = -a b 1, mu_n = N T_n(-a b)."""
+    rng = np.random.default_rng(3)
+    n = 50_001
+    lam = rng.uniform(-4.0, 4.0, n)
+    rp = np.arange(n + 1, dtype=np.int64)
+    col = np.arange(n, dtype=np.int64)
+    a, b, M = 0.9 / 4.5, 0.3, 200
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(rp, col, lam.astype(np.complex128), a, b)
+        mu, _ = ctx.moments(M, R, SEED)
+    x = a * (lam - b)
+    ref = np.array([np.cos(k * np.arccos(x)).sum() for k in range(M)])
+    assert mu[0] == n
+    assert np.max(np.abs(mu - ref)) / n <= TOL
+    n0 = 1000
+    with pkg.KpmContext() as ctx:
+        ctx.set_matrix(np.zeros(n0 + 1, dtype=np.int64), np.zeros(0, dtype=np.int64), np.zeros(0, dtype=np.complex128),
+                       0.5, 1.2)
+        mu, _ = ctx.moments(40, R, SEED)
+    ref0 = n0 * np.cos(np.arange(40) * np.arccos(-0.5 * 1.2))
+    assert np.max(np.abs(mu - ref0)) / n0 <= TOL

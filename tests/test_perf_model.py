@@ -50,4 +50,5 @@ def test_both_arms_emit_the_same_config(bench):
         w = bench.workload(args, world)
         c = bench.config_dict(w, world)
         assert c["workload"] == w["name"] and c["parallelism"] == f"x-slab dp{world}"
-        assert set(c) == {"workload", "lattice", "M", "R", "parallelism"}
+        assert set(c) == {"workload", "lattice", "M", "R", "parallelism", "l2"}
+        assert c["l2"].startswith("no flush: inputs larger than L2")  # C3 slabs, C4: GBs per GPU
