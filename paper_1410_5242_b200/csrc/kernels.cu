@@ -111,9 +111,11 @@ __device__ __forceinline__ double2 ld_stream(const double2* ptr, uint64_t pol) {
   return r;
 }
 __device__ __forceinline__ void st_stream(double2* ptr, double2 v, uint64_t pol) {
+  // no "memory" clobber: nothing in a sweep reads back a W row it stored (the old W rows are read
+  // before, by the TMA fill of the same tile), and the clobber made the compiler reload every
+  // kernel parameter after each store
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(ptr), "d"(v.x), "d"(v.y),
-               "l"(pol)
-               : "memory");
+               "l"(pol));
 }
 
 // Fused halo exchange: a boundary row's new value also goes straight into the neighbour's
@@ -482,6 +484,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
 
   Dots<CPL> d;
   d.zero();
+  const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);  // barrier s at +8 s
   if (warp == NCW) {
     // ---------------- producer warp: TMA bulk copies of tile k into stage k % S ----------
     // Lane i < 16 holds slot i of the chunk's copy record (header + up to 15 bulk copies);
@@ -491,7 +494,11 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
     int64_t c_nxt = my_tiles > 0 ? chunk_at(a, blockIdx.x) : 0;
     uint4 nxt = my_tiles > 0 && lane < 16 ? __ldg(a.rec + (BC ? (int64_t)blockIdx.x : c_nxt) * 16 + lane)
                                           : make_uint4(0u, 0u, 0u, 0u);
-    for (int64_t k = 0; k < my_tiles; ++k) {
+    // ring stage s = k mod S and its round r = k div S, kept incrementally (a runtime 64-bit
+    // division per tile cost ~27 instructions per warp and tile)
+    int s = 0;
+    uint32_t rnd = 0;
+    for (int64_t k = 0; k < my_tiles; ++k, s = (s + 1 == tl.stages) ? 0 : s + 1, rnd += (s == 0)) {
       const uint4 cur = nxt;
       const int64_t c_cur = c_nxt;
       if (k + 1 < my_tiles) {
@@ -499,14 +506,13 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
         const int64_t ri = BC ? blockIdx.x + (k + 1) * gridDim.x : c_nxt;
         nxt = lane < 16 ? __ldg(a.rec + ri * 16 + lane) : make_uint4(0u, 0u, 0u, 0u);
       }
-      const int s = (int)(k % tl.stages);
       const uint32_t total = __shfl_sync(0xffffffffu, W_TILE ? cur.x : cur.y, 0);
       const uint32_t L = __shfl_sync(0xffffffffu, cur.z, 0);
       const uint32_t hw = __shfl_sync(0xffffffffu, cur.w, 0);
       const uint32_t ncmd = BC ? (hw & 0xFFu) : hw;
-      if (k >= tl.stages) mbar_wait(smem_u32(&empty[s]), (uint32_t)(((k / tl.stages) - 1) & 1));
+      if (rnd > 0) mbar_wait(empty0 + 8 * s, (rnd - 1) & 1u);
       unsigned char* st = BC ? tsm : tsm + (size_t)s * tl.stage_bytes;  // BC records: absolute offsets
-      const uint32_t bar = smem_u32(&full[s]);
+      const uint32_t bar = full0 + 8 * s;
       if (lane == 0) {
         tile_len[s] = (int)L;
         tile_own[s] = BC ? (int)(hw >> 8) : 0;
@@ -537,14 +543,15 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
     // blocks in the order cc ^ (q mod 8/LPR), so the rows of a phase cover one 128-B window.
     constexpr int SWR = (LPR < 8 && CPL * LPR >= 8) ? 8 / LPR : 1;
     const int sw = q % SWR;
-    for (int64_t k = 0; k < my_tiles; ++k) {
-      const int s = (int)(k % tl.stages);
+    int s = 0;
+    uint32_t rnd = 0;
+    for (int64_t k = 0; k < my_tiles; ++k, s = (s + 1 == tl.stages) ? 0 : s + 1, rnd += (s == 0)) {
       const unsigned char* st = tsm + (size_t)tl.pool_bytes + (size_t)s * tl.stage_bytes;
       const double2* sV = reinterpret_cast<const double2*>(BC ? tsm : st);
       const double2* sW = reinterpret_cast<const double2*>(st + tl.off_w);
       const double2* sval = reinterpret_cast<const double2*>(st + tl.off_val);
       const uint16_t* slc = reinterpret_cast<const uint16_t*>(st + tl.off_lcol);
-      mbar_wait(smem_u32(&full[s]), (uint32_t)((k / tl.stages) & 1));
+      mbar_wait(full0 + 8 * s, rnd & 1u);
       const int L = tile_len[s];
       const int own_row = tile_own[s];  // 0 unless BC
       const int64_t c = tile_chunk[s];
@@ -616,11 +623,12 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
           for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h, sVt[li + (cc ^ sw) * LPR]);
         }
         if (p < a.n_loc) {
+          double2* const wrow = a.W + p * R;
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) {
             const int col = (cc ^ sw) * LPR + t;
             if (KIND == kSpmmv) {
-              st_stream(a.W + p * R + col, u[cc], pol);
+              st_stream(wrow + col, u[cc], pol);
               continue;
             }
             const double2 vi_c = own0 ? x0[cc] : sV[(own_row + kr) * R + col];
@@ -634,8 +642,8 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
               const double2 wo = WS ? sW[kr * R + col] : wreg[cc];
               w = make_double2(fma(a.scale, uu.x, -wo.x), fma(a.scale, uu.y, -wo.y));
             }
-            st_stream(a.W + p * R + col, w, pol);
-            store_peers<R>(a, p, col, w);
+            st_stream(wrow + col, w, pol);
+            if (a.n_peer) store_peers<R>(a, p, col, w);
             if (KIND == kAug) {
               d.ee[cc] = fma(vi_c.x, vi_c.x, fma(vi_c.y, vi_c.y, d.ee[cc]));
               d.eor[cc] = fma(w.x, vi_c.x, fma(w.y, vi_c.y, d.eor[cc]));
@@ -645,7 +653,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&empty[s]));  // stage s released by this warp
+      if (lane == 0) mbar_arrive(empty0 + 8 * s);  // stage s released by this warp
     }
     // undo the swizzle so that accumulator cc holds column block cc on every lane
     if (SWR > 1 && KIND == kAug) {
