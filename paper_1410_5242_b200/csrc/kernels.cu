@@ -450,7 +450,7 @@ __host__ __device__ constexpr int tiled_threads() { return 32 * (tiled_ncwg<LPR>
 // smaller ring is meant to fit two CTAs per SM).
 // BC: block-cache feed: records per list position, V rows of a tile live in a
 // pool of 32-row blocks kept across the CTA's tiles (plus per-stage extra rows), lcol holds
-// absolute shared-memory V rows, the header carries the own block's first row.
+// absolute shared-memory V rows (times R), the header carries the own block's first row.
 template <int R, int LPR, int U, int CS, bool WS, bool INIT, int KIND = kAug, int MINB = 1, bool BC = false>
 __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tiled(const SweepArgs a) {
   using Cf = Cfg<R, LPR, U>;
@@ -543,6 +543,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
     // blocks in the order cc ^ (q mod 8/LPR), so the rows of a phase cover one 128-B window.
     constexpr int SWR = (LPR < 8 && CPL * LPR >= 8) ? 8 / LPR : 1;
     const int sw = q % SWR;
+    const bool peers = a.n_peer > 0;  // fused halo stores of this launch (edge chunks only)
     int s = 0;
     uint32_t rnd = 0;
     for (int64_t k = 0; k < my_tiles; ++k, s = (s + 1 == tl.stages) ? 0 : s + 1, rnd += (s == 0)) {
@@ -569,7 +570,17 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
         const double2* sv = sval + kr;
         const int lts = BC ? tl.lt_stride : 0;  // row-major tile indices (TileLayout::lt_stride)
         const uint16_t* sl = lts ? slc + kr * lts : slc + kr;
+        constexpr int LM = BC ? 1 : R;  // block-cache tile indices are stored pre-multiplied by R
         const double2* sVt = sV + t;
+        // gather address = this lane's base + 16 * index (one IMAD per gathered row; written this way
+        // the compiler stops folding t into every index)
+        const uint32_t vbase = smem_u32(sVt);
+        auto vat = [&](int li, int cc) -> double2 {
+          double2 r;
+          asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y)
+                       : "r"(vbase + (uint32_t)(li + (cc ^ sw) * LPR) * 16u));
+          return r;
+        };
         int j = 0;
         // The SELL order puts a row's own-position (diagonal) entry first, if stored (DESIGN.md
         // R18): then entry 0's gather is the own row V_i, which the epilogue needs as well, so
@@ -582,15 +593,18 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
         int li0 = -1;
         if (L > 0) {  // uniform per tile
           const double2 h0 = sv[0];
-          li0 = (lts ? sl[lts - 4] : sl[0]) * R;
+          li0 = (lts ? sl[lts - 4] : sl[0]) * LM;
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) {
-            x0[cc] = sVt[li0 + (cc ^ sw) * LPR];
+            x0[cc] = vat(li0, cc);
             cmac(u[cc], h0, x0[cc]);
           }
           j = 1;
         }
-        const bool own0 = PEEL && li0 == (own_row + kr) * R;
+        if (PEEL && li0 != (own_row + kr) * R) {  // entry 0 is not the diagonal: x0 <- V_i
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) x0[cc] = sV[(own_row + kr) * R + (cc ^ sw) * LPR + t];
+        }
         for (; j + U <= L; j += U) {  // full batches: no predication
           double2 h[U];
           int li[U];
@@ -598,19 +612,19 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
           for (int uu = 0; uu < U; ++uu) h[uu] = sv[(j + uu) * kC];
           if (U == 4 && lts && ((j - 1) & 3) == 0) {  // one 8-byte load: entries j..j+3
             const uint2 q4 = *reinterpret_cast<const uint2*>(sl + (j - 1));
-            li[0] = (int)(q4.x & 0xFFFFu) * R;
-            li[1 % U] = (int)(q4.x >> 16) * R;
-            li[2 % U] = (int)(q4.y & 0xFFFFu) * R;
-            li[3 % U] = (int)(q4.y >> 16) * R;
+            li[0] = (int)(q4.x & 0xFFFFu) * LM;
+            li[1 % U] = (int)(q4.x >> 16) * LM;
+            li[2 % U] = (int)(q4.y & 0xFFFFu) * LM;
+            li[3 % U] = (int)(q4.y >> 16) * LM;
           } else {
 #pragma unroll
-            for (int uu = 0; uu < U; ++uu) li[uu] = (lts ? sl[j + uu - 1] : sl[(j + uu) * kC]) * R;
+            for (int uu = 0; uu < U; ++uu) li[uu] = (lts ? sl[j + uu - 1] : sl[(j + uu) * kC]) * LM;
           }
           double2 x[U][CPL];
 #pragma unroll
           for (int uu = 0; uu < U; ++uu)
 #pragma unroll
-            for (int cc = 0; cc < CPL; ++cc) x[uu][cc] = sVt[li[uu] + (cc ^ sw) * LPR];
+            for (int cc = 0; cc < CPL; ++cc) x[uu][cc] = vat(li[uu], cc);
 #pragma unroll
           for (int uu = 0; uu < U; ++uu)
 #pragma unroll
@@ -618,9 +632,9 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
         }
         for (; j < L; ++j) {
           const double2 h = sv[j * kC];
-          const int li = (lts ? sl[j - 1] : sl[j * kC]) * R;
+          const int li = (lts ? sl[j - 1] : sl[j * kC]) * LM;
 #pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h, sVt[li + (cc ^ sw) * LPR]);
+          for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h, vat(li, cc));
         }
         if (p < a.n_loc) {
           double2* const wrow = a.W + p * R;
@@ -631,7 +645,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
               st_stream(wrow + col, u[cc], pol);
               continue;
             }
-            const double2 vi_c = own0 ? x0[cc] : sV[(own_row + kr) * R + col];
+            const double2 vi_c = PEEL ? x0[cc] : sV[(own_row + kr) * R + col];
             double2 uu = u[cc];
             uu.x = fma(-a.b, vi_c.x, uu.x);
             uu.y = fma(-a.b, vi_c.y, uu.y);
@@ -643,7 +657,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
               w = make_double2(fma(a.scale, uu.x, -wo.x), fma(a.scale, uu.y, -wo.y));
             }
             st_stream(wrow + col, w, pol);
-            if (a.n_peer) store_peers<R>(a, p, col, w);
+            if (peers) store_peers<R>(a, p, col, w);
             if (KIND == kAug) {
               d.ee[cc] = fma(vi_c.x, vi_c.x, fma(vi_c.y, vi_c.y, d.ee[cc]));
               d.eor[cc] = fma(w.x, vi_c.x, fma(w.y, vi_c.y, d.eor[cc]));

@@ -164,7 +164,7 @@ int build_sell_device(const int64_t* rp, const int64_t* col, const double2* val,
                       std::string& err, cudaStream_t s);
 // Copy records of the tiled feed for block width R from the per-chunk run lists.
 // Block-cache feed: per-position copy records (kRecSlots uint4, list position b + G k = CTA b's
-// k-th tile) from a simulation of each CTA's pool of 32-row V blocks, and the tile-row index
+// k-th tile) from a simulation of each CTA's pool of 32-row V blocks, and the tile-row index (times R)
 // of every SELL slot pointing into that CTA's shared memory.  *fail != 0 if some tile does not fit.
 cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* runs, const int* scol,
                             const int64_t* list, int64_t n_chunks, int grid, int R, bool with_w,

@@ -395,7 +395,7 @@ __global__ void bc_plan_kernel(const int64_t* __restrict__ cptr, const int* __re
 // Tile-row index (absolute shared-memory V row) of every SELL slot, one warp per tile.
 __global__ void bc_lcol_kernel(const int* __restrict__ scol, const int64_t* __restrict__ cptr,
                                const int64_t* __restrict__ list, int64_t n_chunks, const int* __restrict__ map,
-                               uint16_t* __restrict__ lcol, int* __restrict__ fail, int lts) {
+                               uint16_t* __restrict__ lcol, int* __restrict__ fail, int lts, int R) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t pos = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); pos < n_chunks; pos += warps) {
@@ -409,6 +409,9 @@ __global__ void bc_lcol_kernel(const int* __restrict__ scol, const int64_t* __re
         if (m[1 + 2 * i] == (g >> 5)) row = m[2 + 2 * i] + (g & 31);
       for (int i = 0; i < nx && row < 0; ++i)
         if (g >= m[16 + 3 * i] && g < m[16 + 3 * i] + m[17 + 3 * i]) row = m[18 + 3 * i] + g - m[16 + 3 * i];
+      // stored as row * R (the V row's offset in double2 units, < 227 KB / 16): the sweep adds it to
+      // its lane's base address without a multiply
+      row = row < 0 ? -1 : row * R;
       if (row < 0 || row > 65535) atomicOr(fail, 2);
       if (lts) {  // row-major: entries 1.. at k*lts + j - 1, entry 0 at k*lts + lts - 4
         const int64_t off = e - cptr[c];
@@ -435,7 +438,7 @@ cudaError_t launch_build_bc(const int64_t* cptr, const int* nruns, const int* ru
   bc_plan_kernel<<<(grid + 63) / 64, 64, 0, s>>>(cptr, nruns, runs, list, n_chunks, grid, R, with_w ? 1 : 0, tl, rec,
                                                   map, fail);
   bc_lcol_kernel<<<grid_for(n_chunks * 32, 256), 256, 0, s>>>(scol, cptr, list, n_chunks, map, lcol_bc, fail,
-                                                               tl.lt_stride);
+                                                               tl.lt_stride, R);
   return cudaGetLastError();
 }
 
