@@ -569,7 +569,10 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
         for (int cc = 0; cc < CPL; ++cc) u[cc] = make_double2(0.0, 0.0);
         const double2* sv = sval + kr;
         const int lts = BC ? tl.lt_stride : 0;  // row-major tile indices (TileLayout::lt_stride)
-        const uint16_t* sl = lts ? slc + kr * lts : slc + kr;
+        // RMC: the row-major tile-index path fixed at compile time (block-cache kernels without a
+        // multi-CTA register cap: -2 % at R = 32; at R = 16 the runtime test measured faster)
+        constexpr bool RMC = BC && MINB == 1;
+        const uint16_t* sl = (RMC || lts) ? slc + kr * lts : slc + kr;
         constexpr int LM = BC ? 1 : R;  // block-cache tile indices are stored pre-multiplied by R
         const double2* sVt = sV + t;
         // gather address = this lane's base + 16 * index (one IMAD per gathered row; written this way
@@ -593,7 +596,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
         int li0 = -1;
         if (L > 0) {  // uniform per tile
           const double2 h0 = sv[0];
-          li0 = (lts ? sl[lts - 4] : sl[0]) * LM;
+          li0 = ((RMC || lts) ? sl[lts - 4] : sl[0]) * LM;
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) {
             x0[cc] = vat(li0, cc);
@@ -610,7 +613,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
           int li[U];
 #pragma unroll
           for (int uu = 0; uu < U; ++uu) h[uu] = sv[(j + uu) * kC];
-          if (U == 4 && lts && ((j - 1) & 3) == 0) {  // one 8-byte load: entries j..j+3
+          if (U == 4 && (RMC || (lts && ((j - 1) & 3) == 0))) {  // one 8-byte load: entries j..j+3
             const uint2 q4 = *reinterpret_cast<const uint2*>(sl + (j - 1));
             li[0] = (int)(q4.x & 0xFFFFu) * LM;
             li[1 % U] = (int)(q4.x >> 16) * LM;
@@ -618,7 +621,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
             li[3 % U] = (int)(q4.y >> 16) * LM;
           } else {
 #pragma unroll
-            for (int uu = 0; uu < U; ++uu) li[uu] = (lts ? sl[j + uu - 1] : sl[(j + uu) * kC]) * LM;
+            for (int uu = 0; uu < U; ++uu) li[uu] = ((RMC || lts) ? sl[j + uu - 1] : sl[(j + uu) * kC]) * LM;
           }
           double2 x[U][CPL];
 #pragma unroll
@@ -632,7 +635,7 @@ __global__ void __launch_bounds__(tiled_threads<LPR, CS>(), MINB) aug_spmmv_tile
         }
         for (; j < L; ++j) {
           const double2 h = sv[j * kC];
-          const int li = (lts ? sl[j - 1] : sl[j * kC]) * LM;
+          const int li = ((RMC || lts) ? sl[j - 1] : sl[j * kC]) * LM;
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) cmac(u[cc], h, vat(li, cc));
         }

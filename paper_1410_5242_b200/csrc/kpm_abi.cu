@@ -1128,9 +1128,10 @@ static kpm_status select_variant(kpm_ctx* ctx, int Rk, int& variant, TileLayout&
     const int bcc = variant_bc(Rk, v);
     kpm_status st;
     if (bcc) {
-      pl = s.tiles_ok ? plan_tiles_bc(Rk, s.max_width, variant_wstage(Rk, v), variant_stages(Rk, v), bcc,
-                                      ctx->lcol_t)
-                      : TileLayout();
+      // the block-cache kernels read row-major tile indices only (KPM_LCOL_T=0 turns them off)
+      pl = s.tiles_ok && ctx->lcol_t ? plan_tiles_bc(Rk, s.max_width, variant_wstage(Rk, v), variant_stages(Rk, v), bcc,
+                                                     true)
+                                     : TileLayout();
       ok = pl.stages >= 1;
     } else if (variant_tiled(Rk, v)) {
       if ((st = plan_tiled_feed(ctx, Rk, variant_wstage(Rk, v), variant_stages(Rk, v), pl)) != KPM_OK) return st;
